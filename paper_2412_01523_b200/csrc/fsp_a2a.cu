@@ -1,0 +1,165 @@
+// fsp_a2a.cu — Ulysses all-to-all inside one SP group over NVSwitch peer memory.
+//
+// Eq. (2) AlltoAll(Q_s, K_s, V_s): sequence-sharded -> head-sharded, and Eq. (4)
+// AlltoAll(P_h): head-sharded -> sequence-sharded.  The paper runs
+// these with NCCL on a cached group pool.  Here a group is just
+// a rank range whose receive buffers are mapped into every member (symmetric memory):
+// each rank pushes its slices straight into the peers' receive buffers with 16-byte
+// stores over NVLink, so there is no communicator per group and "hot switching" between
+// plans costs nothing.  The pack (loader-order -> group-packed rows) is fused into the
+// send by reading source rows through the permutation; the unpack is fused into the
+// receive side of head2seq the same way.
+#include "fsp_host.h"
+
+namespace fsp {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxDegree = 8;
+
+struct PeerPtrs {
+  uint8_t* p[kMaxDegree];
+};
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Index space (j, i, m, v): destination peer j outermost so a contiguous range of
+// vectors lands in one peer buffer as one long run; i = shard row, m = matrix (q/k/v),
+// v = 16-byte vector inside the (H/d)*D head slice.
+template <bool kSeq2Head>
+__global__ void __launch_bounds__(kThreads) a2a_kernel(const uint8_t* __restrict__ src,
+                                                       PeerPtrs dst, const int32_t* __restrict__ index,
+                                                       FspA2A a) {
+  const int d = a.degree;
+  const int64_t slice_bytes = (int64_t)(a.n_heads / d) * a.head_dim * 2;
+  const uint32_t vpc = (uint32_t)(slice_bytes / 16);
+  const int64_t per_peer = (int64_t)a.rows_per_rank * a.n_mats * vpc;
+  const int64_t total = per_peer * d;
+  const int64_t src_stride = a.src_stride * 2, dst_stride = a.dst_stride * 2;
+  const int64_t full_row = (int64_t)a.n_heads * a.head_dim * 2;  // bytes of all heads of one mat
+  for (int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * kThreads) {
+    const int j = (int)(g / per_peer);
+    int64_t rem = g - (int64_t)j * per_peer;
+    const uint32_t v = (uint32_t)(rem % vpc);
+    rem /= vpc;
+    const int m = (int)(rem % a.n_mats);
+    const int i = (int)(rem / a.n_mats);
+    if (kSeq2Head) {
+      // local shard row i (all heads) -> peer j row (rank*R + i), head slice j
+      const int32_t srow = index ? index[i] : i;
+      int4 val = make_int4(0, 0, 0, 0);
+      if (srow >= 0)
+        val = ld_stream(reinterpret_cast<const int4*>(src + (int64_t)srow * src_stride +
+                                                      m * full_row + j * slice_bytes) + v);
+      const int64_t drow = (int64_t)a.rank * a.rows_per_rank + i;
+      *(reinterpret_cast<int4*>(dst.p[j] + drow * dst_stride + m * slice_bytes) + v) = val;
+    } else {
+      // local row (j*R + i), own head slice -> peer j shard row i at head slice `rank`
+      const int64_t srow = (int64_t)j * a.rows_per_rank + i;
+      const int32_t drow = index ? index[(int64_t)j * a.rows_per_rank + i] : i;
+      if (drow < 0) continue;
+      const int4 val =
+          ld_stream(reinterpret_cast<const int4*>(src + srow * src_stride + m * slice_bytes) + v);
+      *(reinterpret_cast<int4*>(dst.p[j] + (int64_t)drow * dst_stride + m * full_row +
+                                a.rank * slice_bytes) + v) = val;
+    }
+  }
+  // make the peer stores visible system-wide before the group barrier publishes
+  __threadfence_system();
+}
+
+__global__ void group_barrier_kernel(PeerPtrs sig, int degree, int rank, int slot_base,
+                                     uint32_t epoch) {
+  const int t = threadIdx.x;
+  if (t < degree) {
+    __threadfence_system();
+    uint32_t* slot = reinterpret_cast<uint32_t*>(sig.p[t]) + slot_base + rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(sig.p[rank]) + slot_base + t;
+    uint32_t seen;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(mine) : "memory");
+    } while ((int32_t)(seen - epoch) < 0);
+  }
+  __syncwarp();
+}
+
+int check_a2a(const FspA2A* a, const void* src, void* const* peer_dst) {
+  FSP_CHECK_ARG(a && src && peer_dst, "null pointer argument");
+  FSP_CHECK_ARG(a->degree >= 1 && a->degree <= kMaxDegree && (a->degree & (a->degree - 1)) == 0,
+                "degree must be a power of two in [1, 8] (got %d)", a->degree);
+  FSP_CHECK_ARG(a->rank >= 0 && a->rank < a->degree, "rank %d outside group of %d", a->rank,
+                a->degree);
+  FSP_CHECK_ARG(a->n_heads % a->degree == 0, "n_heads (%d) not divisible by degree (%d)",
+                a->n_heads, a->degree);
+  FSP_CHECK_ARG(a->rows_per_rank >= 0 && a->n_mats >= 1 && a->head_dim >= 8, "bad sizes");
+  FSP_CHECK_ARG(((int64_t)(a->n_heads / a->degree) * a->head_dim * 2) % 16 == 0,
+                "head slice must be a multiple of 16 bytes");
+  FSP_CHECK_ARG(a->src_stride % 8 == 0 && a->dst_stride % 8 == 0, "strides must be multiples of 8");
+  for (int j = 0; j < a->degree; ++j)
+    FSP_CHECK_ARG(peer_dst[j] != nullptr && ((uintptr_t)peer_dst[j] & 15) == 0,
+                  "peer_dst[%d] null or misaligned", j);
+  return FSP_OK;
+}
+
+template <bool kSeq2Head>
+int launch_a2a(const FspA2A* a, const void* src, void* const* peer_dst, const int32_t* index,
+               void* stream) {
+  int rc = check_a2a(a, src, peer_dst);
+  if (rc) return rc;
+  const int64_t full = (int64_t)a->n_heads * a->head_dim * a->n_mats;
+  const int64_t slice = full / a->degree;
+  if (kSeq2Head)
+    FSP_CHECK_ARG(a->src_stride >= full && a->dst_stride >= slice, "strides too small");
+  else
+    FSP_CHECK_ARG(a->src_stride >= slice && a->dst_stride >= full, "strides too small");
+  PeerPtrs pp{};
+  for (int j = 0; j < a->degree; ++j) pp.p[j] = reinterpret_cast<uint8_t*>(peer_dst[j]);
+  const int64_t vecs = (int64_t)a->rows_per_rank * a->n_mats * a->degree *
+                       ((int64_t)(a->n_heads / a->degree) * a->head_dim * 2 / 16);
+  if (vecs == 0) return FSP_OK;
+  int64_t blocks = (vecs + kThreads - 1) / kThreads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  a2a_kernel<kSeq2Head><<<(unsigned)blocks, kThreads, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const uint8_t*>(src), pp, index, *a);
+  FSP_LAUNCH_CHECK();
+  return FSP_OK;
+}
+
+}  // namespace
+}  // namespace fsp
+
+extern "C" int fsp_a2a_seq2head(const FspA2A* a, const void* src, void* const* peer_dst,
+                                const int32_t* d_src_index, void* stream) {
+  return fsp::launch_a2a<true>(a, src, peer_dst, d_src_index, stream);
+}
+
+extern "C" int fsp_a2a_head2seq(const FspA2A* a, const void* src, void* const* peer_dst,
+                                const int32_t* d_dst_index, void* stream) {
+  return fsp::launch_a2a<false>(a, src, peer_dst, d_dst_index, stream);
+}
+
+extern "C" int fsp_group_barrier(uint32_t* const* peer_signal, int32_t degree, int32_t rank,
+                                 int32_t slot_base, uint32_t epoch, void* stream) {
+  using namespace fsp;
+  FSP_CHECK_ARG(peer_signal != nullptr, "null peer_signal");
+  FSP_CHECK_ARG(degree >= 1 && degree <= kMaxDegree, "degree out of range");
+  FSP_CHECK_ARG(rank >= 0 && rank < degree, "rank out of range");
+  FSP_CHECK_ARG(slot_base >= 0, "slot_base must be >= 0");
+  if (degree == 1) return FSP_OK;
+  PeerPtrs pp{};
+  for (int j = 0; j < degree; ++j) {
+    FSP_CHECK_ARG(peer_signal[j] != nullptr, "peer_signal[%d] null", j);
+    pp.p[j] = reinterpret_cast<uint8_t*>(peer_signal[j]);
+  }
+  group_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(pp, degree, rank, slot_base, epoch);
+  FSP_LAUNCH_CHECK();
+  return FSP_OK;
+}

@@ -1,0 +1,387 @@
+// fsp_attn_fwd.cu — packed varlen causal attention forward on tcgen05/TMEM.
+//
+// Eq. (3) of the paper, P_h = softmax(Q_h K_h^T / sqrt(D)) V_h per head slice
+// (PAPER.md:339), with flash-attn varlen semantics: every sequence of
+// the cu_seqlens-packed group attends causally to itself only.
+//
+// One CTA = one 128-row query tile of one sequence x one head.  Warp roles:
+//   warp 0      TMA producer: Q once, then K_j / V_j through a 2-stage ring
+//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T (SS, both K-major SW128),
+//               O += P_j V_j (TS: P from TMEM, V MN-major SW128)
+//   warps 2..5  softmax: one thread per query row; S row from TMEM, online softmax
+//               in exp2 domain, P (bf16) back to TMEM, lazy O rescale, epilogue.
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O [256,256+D) P0 [384,448) P1 [448,512).
+// S is double-buffered so QK^T of tile j+1 overlaps the softmax of tile j.
+#include "fsp_host.h"
+#include "fsp_ptx.cuh"
+
+namespace fsp {
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBN = 128;
+constexpr int kFwdThreads = 192;
+constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256, kColP0 = 384, kColP1 = 448;
+
+struct FwdParams {
+  __nv_bfloat16* o;
+  float* lse;
+  int64_t o_stride;
+  const int32_t* cu_seqlens;
+  const int32_t* tiles;
+  int32_t total_rows;
+  int32_t n_heads;
+  float scale_log2;
+};
+
+template <int D>
+struct FwdSmem {
+  static constexpr int kBoxes = D / 64;
+  static constexpr int kTileBytes = 128 * D * 2;  // 128 rows x D bf16
+  static constexpr int kQ = 0;
+  static constexpr int kK = kQ + kTileBytes;
+  static constexpr int kV = kK + 2 * kTileBytes;
+  static constexpr int kBar = kV + 2 * kTileBytes;
+  static constexpr int kBytes = kBar + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+  using L = FwdSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_q = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2]
+  uint64_t* s_free = bars + 11;  // [2]
+  uint64_t* p_full = bars + 13;  // [2]
+  uint64_t* pv_done = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int head = blockIdx.x % p.n_heads;
+  const int tile = p.tiles[blockIdx.x / p.n_heads];
+  const int seq = tile >> 16;
+  const int qt = tile & 0xFFFF;
+  const int seq_start = p.cu_seqlens[seq];
+  const int seqlen = p.cu_seqlens[seq + 1] - seq_start;
+  const int q0 = qt * kBM;
+  const int n_kv = qt + 1;  // causal: kv tiles 0..qt (kBM == kBN)
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_q, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(s_free + i, 4);
+      mbar_init(p_full + i, 4);
+    }
+    mbar_init(pv_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      mbar_expect_tx(bar_q, L::kTileBytes);
+      for (int b = 0; b < L::kBoxes; ++b)
+        tma_load_3d(smem + L::kQ + b * 16384, &tm_q, bar_q, b * 64, head, seq_start + q0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        const int row = seq_start + j * kBN;
+        mbar_wait(k_empty + st, ph ^ 1);
+        mbar_expect_tx(k_full + st, L::kTileBytes);
+        for (int b = 0; b < L::kBoxes; ++b)
+          tma_load_3d(smem + L::kK + st * L::kTileBytes + b * 16384, &tm_k, k_full + st, b * 64,
+                      head, row);
+        mbar_wait(v_empty + st, ph ^ 1);
+        mbar_expect_tx(v_full + st, L::kTileBytes);
+        for (int b = 0; b < L::kBoxes; ++b)
+          tma_load_3d(smem + L::kV + st * L::kTileBytes + b * 16384, &tm_v, v_full + st, b * 64,
+                      head, row);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(kBM, kBN, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(kBM, D, false, true);
+      const uint32_t q_base = smem_u32(smem + L::kQ);
+      const uint32_t k_base = smem_u32(smem + L::kK);
+      const uint32_t v_base = smem_u32(smem + L::kV);
+      mbar_wait(bar_q, 0);
+      tc_fence_after();
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(k_full + st, (j >> 1) & 1);
+        if (j >= 2) mbar_wait(s_free + st, ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + (st ? kColS1 : kColS0);
+        const uint32_t kb = k_base + st * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(d_tmem, make_sdesc_sw128(q_base + off, 16, 1024),
+                 make_sdesc_sw128(kb + off, 16, 1024), idesc_s, kk > 0);
+        }
+        tc_commit(s_full + st);
+        tc_commit(k_empty + st);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_s(j + 1);
+        const int st = j & 1;
+        mbar_wait(v_full + st, (j >> 1) & 1);
+        mbar_wait(p_full + st, (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t vb = v_base + st * L::kTileBytes;
+        const uint32_t p_tmem = tmem + (st ? kColP1 : kColP0);
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          mma_ts(tmem + kColO, p_tmem + kk * 8, make_sdesc_sw128(vb + kk * 2048, 16384, 1024),
+                 idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(pv_done);
+        tc_commit(v_empty + st);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ softmax warps
+    const uint32_t quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_addr = (quad * 32u) << 16;
+    const int q_pos = q0 + row;
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY;  // running max of scaled scores (log2 units)
+    float l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      mbar_wait(s_full + st, (j >> 1) & 1);
+      tc_fence_after();
+      float s[kBN];
+#pragma unroll
+      for (int c = 0; c < kBN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_addr + (st ? kColS1 : kColS0) + c, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(r[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free + st);
+
+      if (j == n_kv - 1) {  // diagonal tile: causal mask
+        const int lim = q_pos - j * kBN;
+#pragma unroll
+        for (int c = 0; c < kBN; ++c)
+          if (c > lim) s[c] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
+      const float m_new = fmaxf(m, mx * sl2);
+      const float corr = ex2(m - m_new);  // m = -inf on the first tile -> 0
+      float sum = 0.f;
+      uint32_t pk[kBN / 2];
+#pragma unroll
+      for (int c = 0; c < kBN; c += 2) {
+        const float p0 = ex2(fmaf(s[c], sl2, -m_new));
+        const float p1 = ex2(fmaf(s[c + 1], sl2, -m_new));
+        sum += p0 + p1;
+        pk[c / 2] = pack_bf16(p0, p1);
+      }
+      l = l * corr + sum;
+      if (j > 0) {
+        // O rescale needs PV_{j-1} retired; it also frees P buffer st (used by PV_{j-2}).
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, m_new > m)) {
+#pragma unroll
+          for (int c = 0; c < D; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + lane_addr + kColO + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+            tmem_st32(tmem + lane_addr + kColO + c, r);
+          }
+        }
+      }
+      m = m_new;
+      const uint32_t p_col = st ? kColP1 : kColP0;
+#pragma unroll
+      for (int c = 0; c < kBN / 2; c += 16) {
+        uint32_t r[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = pk[c + i];
+        tmem_st16(tmem + lane_addr + p_col + c, r);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full + st);
+    }
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(pv_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
+    const bool valid = q_pos < seqlen;
+    __nv_bfloat16* orow = p.o + (int64_t)(seq_start + q_pos) * p.o_stride + (int64_t)head * D;
+#pragma unroll
+    for (int c = 0; c < D; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lane_addr + kColO + c, r);
+      tmem_ld_wait();
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
+          v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+          v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
+          v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
+          *reinterpret_cast<uint4*>(orow + c + i) = v;
+        }
+      }
+    }
+    if (valid)
+      p.lse[(int64_t)head * p.total_rows + seq_start + q_pos] =
+          (m + __log2f(l)) * 0.69314718055994531f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free<512>(tmem);
+}
+
+}  // namespace
+
+// Tensor map over one bf16 operand of a token-major packed buffer:
+// dims {D, H, rows}, strides {D*2 (head), row_stride*2 (token)}, box {64, 1, 128}.
+int make_head_tmap(CUtensorMap* m, const void* base, int64_t row_stride_elems, int n_heads,
+                   int head_dim, int rows) {
+  uint64_t dims[3] = {(uint64_t)head_dim, (uint64_t)n_heads, (uint64_t)rows};
+  uint64_t strides[2] = {(uint64_t)head_dim * 2, (uint64_t)row_stride_elems * 2};
+  uint32_t box[3] = {64, 1, 128};
+  return encode_tmap_bf16(m, base, 3, dims, strides, box);
+}
+
+template <int D>
+static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
+  CUtensorMap tq, tk, tv;
+  int rc;
+  if ((rc = make_head_tmap(&tq, a->q, a->q_stride, a->n_heads, D, a->total_rows))) return rc;
+  if ((rc = make_head_tmap(&tk, a->k, a->k_stride, a->n_heads, D, a->total_rows))) return rc;
+  if ((rc = make_head_tmap(&tv, a->v, a->v_stride, a->n_heads, D, a->total_rows))) return rc;
+  FwdParams p;
+  p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
+  p.lse = a->lse;
+  p.o_stride = a->o_stride;
+  p.cu_seqlens = a->d_cu_seqlens;
+  p.tiles = a->d_tiles;
+  p.total_rows = a->total_rows;
+  p.n_heads = a->n_heads;
+  p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  const int smem = FwdSmem<D>::kBytes + 1024;
+  FSP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int64_t grid = (int64_t)a->n_tiles * a->n_heads;
+  FSP_CHECK_ARG(grid < (1ll << 31), "grid too large");
+  attn_fwd_kernel<D><<<(unsigned)grid, kFwdThreads, smem, stream>>>(tq, tk, tv, p);
+  FSP_LAUNCH_CHECK();
+  return FSP_OK;
+}
+
+int check_attn_common(const void* q, const void* k, const void* v, int64_t qs, int64_t ks,
+                      int64_t vs, const int32_t* cu, const int32_t* tiles, int32_t n_tiles,
+                      int32_t n_seq, int32_t total_rows, int32_t n_heads, int32_t head_dim) {
+  FSP_CHECK_ARG(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128 (got %d)", head_dim);
+  FSP_CHECK_ARG(n_heads >= 1, "n_heads must be >= 1");
+  FSP_CHECK_ARG(n_seq >= 0 && total_rows >= 0 && n_tiles >= 0, "negative sizes");
+  FSP_CHECK_ARG(q && k && v && cu && (tiles || n_tiles == 0), "null pointer argument");
+  FSP_CHECK_ARG(qs >= (int64_t)n_heads * head_dim && ks >= (int64_t)n_heads * head_dim &&
+                    vs >= (int64_t)n_heads * head_dim,
+                "row strides must cover n_heads*head_dim elements");
+  FSP_CHECK_ARG(qs % 8 == 0 && ks % 8 == 0 && vs % 8 == 0, "row strides must be multiples of 8");
+  return FSP_OK;
+}
+
+}  // namespace fsp
+
+extern "C" int32_t fsp_attn_schedule(const int32_t* cu, int32_t n_seq, int32_t reverse_causal,
+                                     int32_t* tiles, int32_t capacity) {
+  using namespace fsp;
+  FSP_CHECK_ARG(cu != nullptr || n_seq == 0, "null cu_seqlens");
+  FSP_CHECK_ARG(n_seq >= 0 && n_seq < 65536, "n_seq must be in [0, 65536)");
+  if (n_seq > 0) FSP_CHECK_ARG(cu[0] == 0, "cu_seqlens[0] must be 0");
+  int64_t n = 0;
+  for (int s = 0; s < n_seq; ++s) {
+    const int len = cu[s + 1] - cu[s];
+    FSP_CHECK_ARG(len >= 0, "cu_seqlens must be non-decreasing (sequence %d)", s);
+    const int nt = (len + kBM - 1) / kBM;
+    FSP_CHECK_ARG(nt < 65536, "sequence %d too long (%d tokens)", s, len);
+    n += nt;
+  }
+  FSP_CHECK_ARG(n < (1ll << 31), "too many tiles");
+  if (!tiles) return (int32_t)n;
+  FSP_CHECK_ARG(capacity >= n, "tile capacity %d < %lld", capacity, (long long)n);
+  // LPT order: the causal cost of forward tile t is t+1 kv tiles; of backward kv tile t
+  // it is (n_tiles - t).  Counting sort by cost, heaviest first; ties by (seq, tile).
+  int max_cost = 0;
+  for (int s = 0; s < n_seq; ++s) {
+    const int nt = (cu[s + 1] - cu[s] + kBM - 1) / kBM;
+    if (nt > max_cost) max_cost = nt;
+  }
+  int64_t* count = new int64_t[max_cost + 2]();
+  for (int s = 0; s < n_seq; ++s) {
+    const int nt = (cu[s + 1] - cu[s] + kBM - 1) / kBM;
+    for (int t = 0; t < nt; ++t) {
+      const int cost = reverse_causal ? nt - t : t + 1;
+      count[max_cost - cost + 1]++;
+    }
+  }
+  for (int c = 1; c <= max_cost + 1; ++c) count[c] += count[c - 1];
+  for (int s = 0; s < n_seq; ++s) {
+    const int nt = (cu[s + 1] - cu[s] + kBM - 1) / kBM;
+    for (int t = 0; t < nt; ++t) {
+      const int cost = reverse_causal ? nt - t : t + 1;
+      tiles[count[max_cost - cost]++] = (s << 16) | t;
+    }
+  }
+  delete[] count;
+  return (int32_t)n;
+}
+
+extern "C" int fsp_attn_fwd(const FspAttnFwd* a, void* stream) {
+  using namespace fsp;
+  FSP_CHECK_ARG(a != nullptr, "null args");
+  int rc = check_attn_common(a->q, a->k, a->v, a->q_stride, a->k_stride, a->v_stride,
+                             a->d_cu_seqlens, a->d_tiles, a->n_tiles, a->n_seq, a->total_rows,
+                             a->n_heads, a->head_dim);
+  if (rc) return rc;
+  FSP_CHECK_ARG(a->o && a->lse, "null output pointer");
+  FSP_CHECK_ARG(a->o_stride >= (int64_t)a->n_heads * a->head_dim && a->o_stride % 8 == 0,
+                "bad o_stride");
+  if (a->n_tiles == 0 || a->total_rows == 0) return FSP_OK;
+  return a->head_dim == 128 ? launch_fwd<128>(a, (cudaStream_t)stream)
+                            : launch_fwd<64>(a, (cudaStream_t)stream);
+}
