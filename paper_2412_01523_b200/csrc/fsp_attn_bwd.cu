@@ -1,10 +1,458 @@
-// fsp_attn_bwd.cu — packed varlen causal attention backward (placeholder until the
-// tcgen05 kernel lands; returns FSP_ERR_UNSUPPORTED so callers fail loudly).
+// fsp_attn_bwd.cu — packed varlen causal attention backward on tcgen05/TMEM.
+//
+// Gradient of Eq. (3) under flash-attn varlen semantics.
+// Three launches:
+//   1. prep:  delta[h,t] = sum_d O[t,h,d] * dO[t,h,d] (fp32) and dq_accum := 0
+//   2. main:  one CTA = one 128-row KV tile of one sequence x one head; loops over the
+//             query tiles that see it causally (i >= kv tile) and keeps dK, dV in TMEM:
+//               S^T  = K Q_i^T            (SS, K-major / K-major)
+//               dP^T = V dO_i^T           (SS)
+//               P^T  = exp2(S^T*scale*log2e - lse2_i)      (registers -> TMEM, bf16)
+//               dS^T = P^T (dP^T - delta_i)                 (registers -> smem, bf16, SW128)
+//               dV  += P^T dO_i           (TS: A = P^T in TMEM, B = dO_i MN-major)
+//               dK  += dS^T Q_i           (SS: A = dS^T K-major, B = Q_i MN-major)
+//               dQ_i = dS K               (SS: A = dS MN-major (same smem), B = K MN-major)
+//             dQ_i is read out of TMEM and added to dq_accum with vector reductions.
+//   3. post:  dq = bf16(dq_accum * scale)
+// TMEM (512 cols): dK [0,128) dV [128,256) S^T|P^T [256,384) dP^T|dQ [384,512).
+// smem: K, V (resident), a 3-slot ring of 32 KB tiles streaming Q_i / dO_i, dS (32 KB).
 #include "fsp_host.h"
+#include "fsp_ptx.cuh"
+
+namespace fsp {
+
+int make_head_tmap(CUtensorMap* m, const void* base, int64_t row_stride_elems, int n_heads,
+                   int head_dim, int rows);
+int check_attn_common(const void* q, const void* k, const void* v, int64_t qs, int64_t ks,
+                      int64_t vs, const int32_t* cu, const int32_t* tiles, int32_t n_tiles,
+                      int32_t n_seq, int32_t total_rows, int32_t n_heads, int32_t head_dim);
+
+namespace {
+
+constexpr int kTile = 128;
+constexpr int kBwdThreads = 192;
+constexpr uint32_t kColDK = 0, kColDV = 128, kColS = 256, kColDP = 384;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct BwdParams {
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  float* dq_accum;
+  const float* lse;
+  const float* delta;
+  int64_t dk_stride, dv_stride;
+  const int32_t* cu_seqlens;
+  const int32_t* tiles;
+  int32_t total_rows;
+  int32_t n_heads;
+  float scale;
+  float scale_log2;
+};
+
+template <int D>
+struct BwdSmem {
+  static constexpr int kBoxes = D / 64;
+  static constexpr int kTileBytes = 128 * D * 2;
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + kTileBytes;
+  static constexpr int kRing = kV + kTileBytes;  // 3 slots
+  static constexpr int kDS = kRing + 3 * kTileBytes;
+  static constexpr int kStat = kDS + 128 * 128 * 2;  // lse2[2][128], delta[2][128]
+  static constexpr int kBar = kStat + 4 * 128 * 4;
+  static constexpr int kBytes = kBar + 256;
+};
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                    const BwdParams p) {
+  using L = BwdSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  float* lse_s = reinterpret_cast<float*>(smem + L::kStat);         // [2][128]
+  float* delta_s = lse_s + 256;                                     // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_kv = bars + 0;
+  uint64_t* ring_full = bars + 1;   // [3]
+  uint64_t* ring_empty = bars + 4;  // [3]
+  uint64_t* s_full = bars + 7;
+  uint64_t* p_ready = bars + 8;
+  uint64_t* dq_full = bars + 9;
+  uint64_t* tm_free = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int head = blockIdx.x % p.n_heads;
+  const int tile = p.tiles[blockIdx.x / p.n_heads];
+  const int seq = tile >> 16;
+  const int kt = tile & 0xFFFF;
+  const int seq_start = p.cu_seqlens[seq];
+  const int seqlen = p.cu_seqlens[seq + 1] - seq_start;
+  const int kv0 = kt * kTile;
+  const int nq = (seqlen + kTile - 1) / kTile;
+  const int n_it = nq - kt;  // query tiles kt .. nq-1
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_kv, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(ring_full + i, 1);
+      mbar_init(ring_empty + i, 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_ready, 4);
+    mbar_init(dq_full, 1);
+    mbar_init(tm_free, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      tma_prefetch(&tm_do);
+      mbar_expect_tx(bar_kv, 2 * L::kTileBytes);
+      for (int b = 0; b < L::kBoxes; ++b) {
+        tma_load_3d(smem + L::kK + b * 16384, &tm_k, bar_kv, b * 64, head, seq_start + kv0);
+        tma_load_3d(smem + L::kV + b * 16384, &tm_v, bar_kv, b * 64, head, seq_start + kv0);
+      }
+      for (int item = 0; item < 2 * n_it; ++item) {
+        const int slot = item % 3;
+        const uint32_t ph = (item / 3) & 1;
+        const int row = seq_start + (kt + (item >> 1)) * kTile;
+        mbar_wait(ring_empty + slot, ph ^ 1);
+        mbar_expect_tx(ring_full + slot, L::kTileBytes);
+        const CUtensorMap* map = (item & 1) ? &tm_do : &tm_q;
+        for (int b = 0; b < L::kBoxes; ++b)
+          tma_load_3d(smem + L::kRing + slot * L::kTileBytes + b * 16384, map, ring_full + slot,
+                      b * 64, head, row);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_dvdk = make_idesc_bf16(128, D, false, true);
+      constexpr uint32_t idesc_dq = make_idesc_bf16(128, D, true, true);
+      const uint32_t k_base = smem_u32(smem + L::kK);
+      const uint32_t v_base = smem_u32(smem + L::kV);
+      const uint32_t ring_base = smem_u32(smem + L::kRing);
+      const uint32_t ds_base = smem_u32(smem + L::kDS);
+      mbar_wait(bar_kv, 0);
+      for (int it = 0; it < n_it; ++it) {
+        const int sq = (2 * it) % 3, sd = (2 * it + 1) % 3;
+        const uint32_t pq = ((2 * it) / 3) & 1, pd = ((2 * it + 1) / 3) & 1;
+        const uint32_t q_base = ring_base + sq * L::kTileBytes;
+        const uint32_t do_base = ring_base + sd * L::kTileBytes;
+        if (it > 0) mbar_wait(tm_free, (it - 1) & 1);
+        mbar_wait(ring_full + sq, pq);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tmem + kColS, make_sdesc_sw128(k_base + off, 16, 1024),
+                 make_sdesc_sw128(q_base + off, 16, 1024), idesc_s, kk > 0);
+        }
+        mbar_wait(ring_full + sd, pd);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tmem + kColDP, make_sdesc_sw128(v_base + off, 16, 1024),
+                 make_sdesc_sw128(do_base + off, 16, 1024), idesc_s, kk > 0);
+        }
+        tc_commit(s_full);
+        mbar_wait(p_ready, it & 1);
+        tc_fence_after();
+        const uint32_t acc = it > 0 ? 1u : 0u;
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)  // dV += P^T dO
+          mma_ts(tmem + kColDV, tmem + kColS + kk * 8,
+                 make_sdesc_sw128(do_base + kk * 2048, 16384, 1024), idesc_dvdk, acc | (kk > 0));
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk) {  // dK += dS^T Q
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tmem + kColDK, make_sdesc_sw128(ds_base + off, 16, 1024),
+                 make_sdesc_sw128(q_base + kk * 2048, 16384, 1024), idesc_dvdk, acc | (kk > 0));
+        }
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)  // dQ = dS K
+          mma_ss(tmem + kColDP, make_sdesc_sw128(ds_base + kk * 2048, 16384, 1024),
+                 make_sdesc_sw128(k_base + kk * 2048, 16384, 1024), idesc_dq, kk > 0);
+        tc_commit(dq_full);
+        tc_commit(ring_empty + sq);
+        tc_commit(ring_empty + sd);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ compute warps
+    const uint32_t quad = warp & 3;
+    const int r = quad * 32 + lane;  // kv row for S^T/dP^T, q row for dQ
+    const uint32_t lane_addr = (quad * 32u) << 16;
+    const int kv_pos = kv0 + r;
+    const float sl2 = p.scale_log2;
+    uint8_t* ds_row = smem + L::kDS + r * 128;  // row r of box 0; box 1 at +16384
+    for (int it = 0; it < n_it; ++it) {
+      const int q0 = (kt + it) * kTile;
+      const int buf = it & 1;
+      {
+        const int t = r;
+        const bool valid = q0 + t < seqlen;
+        const int64_t gi = (int64_t)head * p.total_rows + seq_start + q0 + t;
+        lse_s[buf * 128 + t] = valid ? p.lse[gi] * kLog2e : INFINITY;
+        delta_s[buf * 128 + t] = valid ? p.delta[gi] : 0.f;
+      }
+      named_bar_sync(1, 128);
+      const float* ls = lse_s + buf * 128;
+      const float* dl = delta_s + buf * 128;
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      const bool diag = (it == 0);
+#pragma unroll
+      for (int c = 0; c < kTile; c += 32) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tmem + lane_addr + kColS + c, sr);
+        tmem_ld32(tmem + lane_addr + kColDP + c, dr);
+        tmem_ld_wait();
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p0 = ex2(fmaf(__uint_as_float(sr[i]), sl2, -ls[c + i]));
+          float p1 = ex2(fmaf(__uint_as_float(sr[i + 1]), sl2, -ls[c + i + 1]));
+          if (diag) {  // causal: q_pos >= kv_pos  <=>  (c+i) >= r on the diagonal tile
+            if (c + i < r) p0 = 0.f;
+            if (c + i + 1 < r) p1 = 0.f;
+          }
+          const float d0 = p0 * (__uint_as_float(dr[i]) - dl[c + i]);
+          const float d1 = p1 * (__uint_as_float(dr[i + 1]) - dl[c + i + 1]);
+          pk[i / 2] = pack_bf16(p0, p1);
+          dk[i / 2] = pack_bf16(d0, d1);
+        }
+        tmem_st16(tmem + lane_addr + kColS + c / 2, pk);
+        // dS^T row r, q columns [c, c+32): box c/64, 16-byte chunks ((c%64)/8 + v) ^ (r%8)
+        uint8_t* box = ds_row + (c >> 6) * 16384;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int chunk = (((c & 63) >> 3) + v) ^ (r & 7);
+          *reinterpret_cast<uint4*>(box + chunk * 16) =
+              make_uint4(dk[4 * v], dk[4 * v + 1], dk[4 * v + 2], dk[4 * v + 3]);
+        }
+      }
+      tmem_st_wait();
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+      // ---- dQ_i readout: lane r is query row q0 + r
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      const bool qvalid = q0 + r < seqlen;
+      float* dq_row = p.dq_accum + ((int64_t)(seq_start + q0 + r) * p.n_heads + head) * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t qr[32];
+        tmem_ld32(tmem + lane_addr + kColDP + c, qr);
+        tmem_ld_wait();
+        if (qvalid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            red_add_v4(dq_row + c + i, __uint_as_float(qr[i]), __uint_as_float(qr[i + 1]),
+                       __uint_as_float(qr[i + 2]), __uint_as_float(qr[i + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tm_free);
+    }
+    // ---- epilogue: dK (scaled), dV for kv row r (TMEM loads are warp-collective)
+    {
+      const bool kvalid = kv_pos < seqlen;
+      __nv_bfloat16* dk_row = p.dk + (int64_t)(seq_start + kv_pos) * p.dk_stride + (int64_t)head * D;
+      __nv_bfloat16* dv_row = p.dv + (int64_t)(seq_start + kv_pos) * p.dv_stride + (int64_t)head * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t a[32], b[32];
+        tmem_ld32(tmem + lane_addr + kColDK + c, a);
+        tmem_ld32(tmem + lane_addr + kColDV + c, b);
+        tmem_ld_wait();
+        if (!kvalid) continue;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 vk, vv;
+          vk.x = pack_bf16(__uint_as_float(a[i]) * p.scale, __uint_as_float(a[i + 1]) * p.scale);
+          vk.y = pack_bf16(__uint_as_float(a[i + 2]) * p.scale, __uint_as_float(a[i + 3]) * p.scale);
+          vk.z = pack_bf16(__uint_as_float(a[i + 4]) * p.scale, __uint_as_float(a[i + 5]) * p.scale);
+          vk.w = pack_bf16(__uint_as_float(a[i + 6]) * p.scale, __uint_as_float(a[i + 7]) * p.scale);
+          vv.x = pack_bf16(__uint_as_float(b[i]), __uint_as_float(b[i + 1]));
+          vv.y = pack_bf16(__uint_as_float(b[i + 2]), __uint_as_float(b[i + 3]));
+          vv.z = pack_bf16(__uint_as_float(b[i + 4]), __uint_as_float(b[i + 5]));
+          vv.w = pack_bf16(__uint_as_float(b[i + 6]), __uint_as_float(b[i + 7]));
+          *reinterpret_cast<uint4*>(dk_row + c + i) = vk;
+          *reinterpret_cast<uint4*>(dv_row + c + i) = vv;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free<512>(tmem);
+}
+
+// delta[h, t] = <O[t,h,:], dO[t,h,:]> in fp32; dq_accum[t,h,:] = 0.  One warp per (t, h).
+template <int D>
+__global__ void __launch_bounds__(256) attn_bwd_prep_kernel(
+    const __nv_bfloat16* __restrict__ o, int64_t o_stride, const __nv_bfloat16* __restrict__ dout,
+    int64_t do_stride, float* __restrict__ delta, float* __restrict__ dq_accum, int total_rows,
+    int n_heads) {
+  constexpr int kPer = D / 32;  // elements per lane (2 or 4)
+  const int64_t n = (int64_t)total_rows * n_heads;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t t = w / n_heads;
+    const int h = (int)(w - t * n_heads);
+    const __nv_bfloat16* op = o + t * o_stride + (int64_t)h * D + lane * kPer;
+    const __nv_bfloat16* dp = dout + t * do_stride + (int64_t)h * D + lane * kPer;
+    float acc = 0.f;
+    if (kPer == 4) {
+      const uint2 a = *reinterpret_cast<const uint2*>(op);
+      const uint2 b = *reinterpret_cast<const uint2*>(dp);
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float2 fa = __bfloat1622float2(a2[i]), fb = __bfloat1622float2(b2[i]);
+        acc += fa.x * fb.x + fa.y * fb.y;
+      }
+    } else {
+      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(op);
+      const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(dp);
+      const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+      acc = fa.x * fb.x + fa.y * fb.y;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    if (lane == 0) delta[(int64_t)h * total_rows + t] = acc;
+    float* dq = dq_accum + (t * n_heads + h) * D + lane * kPer;
+    if (kPer == 4)
+      *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
+    else
+      *reinterpret_cast<float2*>(dq) = make_float2(0.f, 0.f);
+  }
+}
+
+// dq[t, h*D + i] = bf16(dq_accum[t, h, i] * scale); 8 elements per thread.
+__global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restrict__ dq_accum,
+                                                            __nv_bfloat16* __restrict__ dq,
+                                                            int64_t dq_stride, int total_rows,
+                                                            int row_elems, float scale) {
+  const int64_t per_row = row_elems / 8;
+  const int64_t n = (int64_t)total_rows * per_row;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = g / per_row;
+    const int64_t c = (g - t * per_row) * 8;
+    const float4 a = *reinterpret_cast<const float4*>(dq_accum + t * row_elems + c);
+    const float4 b = *reinterpret_cast<const float4*>(dq_accum + t * row_elems + c + 4);
+    uint4 v;
+    v.x = pack_bf16(a.x * scale, a.y * scale);
+    v.y = pack_bf16(a.z * scale, a.w * scale);
+    v.z = pack_bf16(b.x * scale, b.y * scale);
+    v.w = pack_bf16(b.z * scale, b.w * scale);
+    *reinterpret_cast<uint4*>(dq + t * dq_stride + c) = v;
+  }
+}
+
+template <int D>
+int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
+  const int T = a->total_rows, H = a->n_heads;
+  {
+    const int64_t warps = (int64_t)T * H;
+    int64_t blocks = (warps * 32 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    attn_bwd_prep_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(
+        reinterpret_cast<const __nv_bfloat16*>(a->o), a->o_stride,
+        reinterpret_cast<const __nv_bfloat16*>(a->dout), a->do_stride, a->delta, a->dq_accum, T, H);
+    FSP_LAUNCH_CHECK();
+  }
+  if (a->n_tiles > 0) {
+    CUtensorMap tq, tk, tv, tdo;
+    int rc;
+    if ((rc = make_head_tmap(&tq, a->q, a->q_stride, H, D, T))) return rc;
+    if ((rc = make_head_tmap(&tk, a->k, a->k_stride, H, D, T))) return rc;
+    if ((rc = make_head_tmap(&tv, a->v, a->v_stride, H, D, T))) return rc;
+    if ((rc = make_head_tmap(&tdo, a->dout, a->do_stride, H, D, T))) return rc;
+    BwdParams p;
+    p.dk = reinterpret_cast<__nv_bfloat16*>(a->dk);
+    p.dv = reinterpret_cast<__nv_bfloat16*>(a->dv);
+    p.dq_accum = a->dq_accum;
+    p.lse = a->lse;
+    p.delta = a->delta;
+    p.dk_stride = a->dk_stride;
+    p.dv_stride = a->dv_stride;
+    p.cu_seqlens = a->d_cu_seqlens;
+    p.tiles = a->d_tiles;
+    p.total_rows = T;
+    p.n_heads = H;
+    p.scale = a->softmax_scale;
+    p.scale_log2 = a->softmax_scale * kLog2e;
+    const int smem = BwdSmem<D>::kBytes + 1024;
+    FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t grid = (int64_t)a->n_tiles * H;
+    FSP_CHECK_ARG(grid < (1ll << 31), "grid too large");
+    attn_bwd_kernel<D><<<(unsigned)grid, kBwdThreads, smem, stream>>>(tq, tk, tv, tdo, p);
+    FSP_LAUNCH_CHECK();
+  }
+  {
+    const int64_t n = (int64_t)T * H * D / 8;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (n > 0) {
+      attn_bwd_post_kernel<<<(unsigned)blocks, 256, 0, stream>>>(
+          a->dq_accum, reinterpret_cast<__nv_bfloat16*>(a->dq), a->dq_stride, T, H * D,
+          a->softmax_scale);
+      FSP_LAUNCH_CHECK();
+    }
+  }
+  return FSP_OK;
+}
+
+}  // namespace
+}  // namespace fsp
 
 extern "C" int fsp_attn_bwd(const FspAttnBwd* a, void* stream) {
-  (void)a;
-  (void)stream;
-  fsp::set_error("fsp_attn_bwd: not implemented yet");
-  return FSP_ERR_UNSUPPORTED;
+  using namespace fsp;
+  FSP_CHECK_ARG(a != nullptr, "null args");
+  int rc = check_attn_common(a->q, a->k, a->v, a->q_stride, a->k_stride, a->v_stride,
+                             a->d_cu_seqlens, a->d_tiles, a->n_tiles, a->n_seq, a->total_rows,
+                             a->n_heads, a->head_dim);
+  if (rc) return rc;
+  FSP_CHECK_ARG(a->o && a->dout && a->lse && a->dq && a->dk && a->dv && a->dq_accum && a->delta,
+                "null pointer argument");
+  const int64_t hd = (int64_t)a->n_heads * a->head_dim;
+  FSP_CHECK_ARG(a->o_stride >= hd && a->do_stride >= hd && a->dq_stride >= hd &&
+                    a->dk_stride >= hd && a->dv_stride >= hd,
+                "row strides must cover n_heads*head_dim elements");
+  FSP_CHECK_ARG(a->o_stride % 8 == 0 && a->do_stride % 8 == 0 && a->dq_stride % 8 == 0 &&
+                    a->dk_stride % 8 == 0 && a->dv_stride % 8 == 0,
+                "row strides must be multiples of 8");
+  if (a->total_rows == 0) return FSP_OK;
+  return a->head_dim == 128 ? launch_bwd<128>(a, (cudaStream_t)stream)
+                            : launch_bwd<64>(a, (cudaStream_t)stream);
 }

@@ -1,0 +1,52 @@
+"""Quick attention-kernel timing at the C2 shape (dev tool, not the bench)."""
+import sys, os, math, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2412_01523_b200 import ops
+
+def lengths_c2():
+    rng = np.random.default_rng(0)
+    raw = 1024 * (1.0 + rng.pareto(1.1, size=64))
+    return np.clip(np.rint(raw), 1, 32768).astype(int)
+
+def timeit(fn, iters=10, warm=3):
+    for _ in range(warm): fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    for _ in range(iters): fn()
+    e.record(); torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+H, D = int(os.environ.get("H", 32)), 128
+L = lengths_c2()
+cu = np.concatenate([[0], np.cumsum(L)]).astype(np.int32)
+T = int(cu[-1]); ss = float((L.astype(np.float64)**2).sum())
+print("T", T, "sum s^2", ss)
+dev = torch.device("cuda")
+qkv = torch.randn(T, 3, H, D, device=dev, dtype=torch.bfloat16)
+do = torch.randn(T, H, D, device=dev, dtype=torch.bfloat16)
+sched = ops.AttnSchedule.build(cu, dev)
+q, k, v = qkv[:, 0], qkv[:, 1], qkv[:, 2]
+fl_fwd = 2 * D * H * ss  # causal half counted: 4*D*H*s^2/2
+ms = timeit(lambda: ops.attn_fwd(q, k, v, sched))
+print(f"fsp fwd: {ms:.3f} ms  {fl_fwd/ms/1e9:.1f} TFLOP/s")
+try:
+    o, lse = ops.attn_fwd(q, k, v, sched)
+    ms = timeit(lambda: ops.attn_bwd(q, k, v, o, do, lse, sched))
+    print(f"fsp bwd: {ms:.3f} ms  {2.5*fl_fwd/ms/1e9:.1f} TFLOP/s")
+except Exception as ex:
+    print("bwd:", ex)
+try:
+    from flash_attn import flash_attn_varlen_func
+    cu_t = torch.from_numpy(cu).to(dev)
+    qc, kc, vc = q.contiguous(), k.contiguous(), v.contiguous()
+    mx = int(L.max())
+    ms = timeit(lambda: flash_attn_varlen_func(qc, kc, vc, cu_t, cu_t, mx, mx, causal=True))
+    print(f"flash_attn2 fwd: {ms:.3f} ms  {fl_fwd/ms/1e9:.1f} TFLOP/s")
+    qc.requires_grad_(); kc.requires_grad_(); vc.requires_grad_()
+    out = flash_attn_varlen_func(qc, kc, vc, cu_t, cu_t, mx, mx, causal=True)
+    ms = timeit(lambda: torch.autograd.grad(out, (qc, kc, vc), do, retain_graph=True))
+    print(f"flash_attn2 bwd: {ms:.3f} ms  {2.5*fl_fwd/ms/1e9:.1f} TFLOP/s")
+except Exception as ex:
+    print("flash_attn:", ex)
