@@ -1,0 +1,288 @@
+"""FlexSP per-step SP executor: Plan -> pack -> all-to-all -> attention -> all-to-all.
+
+The paper's runtime "sequentially reads one plan per iteration to train",
+"generates the SP communication groups dynamically and scatters the data into the
+corresponding group" and runs Ulysses SP "similar to DeepSpeed-Ulysses"
+ with flash-attn varlen.  The reference package stops at
+the Plan (pkg/src/seqplan/domain.py:381-400); this module is the executor under it.
+
+B200 design:
+* one process per GPU; a single symmetric-memory heap per rank is rendezvoused once
+  (torch.distributed._symmetric_memory) and carved at identical offsets on every rank,
+  so the receive buffer of any rank is `peer_base[r] + offset` — an SP group is just a
+  rank block [r0, r0+d) and switching groups between micro-batches costs nothing
+  (the paper's NCCL group pool, is not needed);
+* pack is fused into the seq->head exchange and unpack into head->seq
+  (fsp_a2a_seq2head / fsp_a2a_head2seq read/write rows through the layout tables);
+* groups of one micro-batch run concurrently on disjoint ranks; micro-batches run in
+  order (gradient accumulation);
+* every exchange ends in a peer-memory flag barrier over the group; a world barrier
+  opens each micro-batch because the rank blocks are regrouped there.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Any, Sequence
+
+import numpy as np
+import torch
+
+from . import ops
+from .profiling import EventTimer
+from .layout import GroupLayout, LayoutError, MicroBatchLayout, build_plan_layouts
+
+_ALIGN = 4096
+_SIGNAL_BYTES = 4096
+
+
+def _align(n: int) -> int:
+    return -(-n // _ALIGN) * _ALIGN
+
+
+class PeerHeap:
+    """One symmetric-memory heap per rank, identical offsets on every rank."""
+
+    def __init__(self, nbytes: int, device: torch.device, world_size: int, group=None):
+        self.device = device
+        self.world_size = world_size
+        self.nbytes = nbytes
+        if world_size == 1:
+            self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+            self.ptrs = [self.buf.data_ptr()]
+        else:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+            self.buf[:_SIGNAL_BYTES].zero_()
+            self.handle = symm_mem.rendezvous(self.buf, group if group is not None
+                                              else dist.group.WORLD)
+            self.ptrs = [int(p) for p in self.handle.buffer_ptrs]
+            torch.cuda.synchronize(device)
+            dist.barrier(group=group)
+
+    def view(self, offset: int, shape: Sequence[int], dtype: torch.dtype) -> torch.Tensor:
+        n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        if offset + n > self.nbytes:
+            raise LayoutError("peer heap too small for this plan")
+        return self.buf[offset:offset + n].view(dtype).view(*shape)
+
+    def peer(self, rank: int, offset: int) -> int:
+        return self.ptrs[rank] + offset
+
+
+@dataclass
+class RankMicroBatch:
+    """This rank's share of one micro-batch."""
+    layout: MicroBatchLayout
+    group: GroupLayout | None
+    j: int                                  # rank inside the group
+    n_local: int                            # loader-order rows this rank holds
+    local_tokens: np.ndarray                # loader token ids of those rows
+    pack_index: torch.Tensor | None = None  # int32 [R]
+    unpack_table: torch.Tensor | None = None  # int32 [d*R]
+    sched: ops.AttnSchedule | None = None
+    fwd_flops: float = 0.0                  # 2 * D * (H/d) * sum s^2 (causal, FA convention)
+
+
+@dataclass
+class StepPlan:
+    """Device-ready form of one Plan for this rank (built once, reused every step)."""
+    strategy: str
+    lengths: list[int]
+    micro_batches: list[RankMicroBatch]
+    offsets: dict[str, int] = field(default_factory=dict)
+    heap_bytes: int = 0
+
+    @property
+    def total_tokens(self) -> int:
+        return int(sum(self.lengths))
+
+
+class FlexSPExecutor:
+    """Runs the SP attention step of a plan on this rank (one process per GPU)."""
+
+    def __init__(self, world_size: int, rank: int, n_heads: int, head_dim: int,
+                 device: torch.device | str = "cuda", softmax_scale: float | None = None,
+                 group=None):
+        if head_dim not in (64, 128):
+            raise ValueError("head_dim must be 64 or 128")
+        self.world_size = world_size
+        self.rank = rank
+        self.n_heads = n_heads
+        self.head_dim = head_dim
+        self.device = torch.device(device)
+        self.scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(head_dim)
+        self.group = group
+        self.heap: PeerHeap | None = None
+        self.epoch = 0
+        self._ws: dict[str, torch.Tensor] = {}
+        self.timer = EventTimer()
+
+    # ------------------------------------------------------------ planning -> tables
+    def prepare(self, plan: Any, lengths: Sequence[int]) -> StepPlan:
+        layouts = build_plan_layouts(plan, lengths, self.world_size, self.n_heads)
+        hd = self.n_heads * self.head_dim
+        mbs: list[RankMicroBatch] = []
+        max_recv = max_local = 0
+        for lay in layouts:
+            grp, j = lay.group_of(self.rank)
+            if grp is None:
+                mbs.append(RankMicroBatch(lay, None, -1, 0, np.zeros(0, dtype=np.int64)))
+            else:
+                local = grp.local_tokens(j)
+                rmb = RankMicroBatch(lay, grp, j, int(local.shape[0]), local)
+                rmb.pack_index = torch.from_numpy(grp.pack_index(j)).to(self.device)
+                rmb.unpack_table = torch.from_numpy(
+                    np.ascontiguousarray(grp.unpack_table().reshape(-1))).to(self.device)
+                rmb.sched = ops.AttnSchedule.build(grp.cu_seqlens, self.device,
+                                                   total_rows=grp.padded_tokens)
+                seg = np.diff(grp.cu_seqlens).astype(np.float64)
+                rmb.fwd_flops = 2.0 * self.head_dim * (self.n_heads // grp.degree) * float((seg ** 2).sum())
+                mbs.append(rmb)
+            # heap regions must be identical on every rank: size by the max over ranks
+            for g in lay.groups:
+                max_recv = max(max_recv, g.padded_tokens * (hd // g.degree))
+                for jj in range(g.degree):
+                    max_local = max(max_local, int((g.shard(jj) >= 0).sum()))
+        off = {}
+        cur = _SIGNAL_BYTES
+        for name, elems in (("qkv_recv", 3 * max_recv), ("out_local", max_local * hd),
+                            ("do_recv", max_recv), ("dqkv_local", 3 * max_local * hd)):
+            off[name] = cur
+            cur += _align(max(elems, 1) * 2)
+        strategy = plan["strategy"] if isinstance(plan, dict) else getattr(plan, "strategy", "")
+        sp = StepPlan(strategy, [int(s) for s in lengths], mbs, off, cur)
+        self._ensure_heap(cur)
+        return sp
+
+    def _ensure_heap(self, nbytes: int) -> None:
+        if self.heap is not None and self.heap.nbytes >= nbytes:
+            return
+        # collective when world_size > 1: every rank prepares the same plan
+        self.heap = PeerHeap(nbytes, self.device, self.world_size, self.group)
+        self.epoch = 0
+
+    def _workspace(self, name: str, numel: int, dtype: torch.dtype) -> torch.Tensor:
+        t = self._ws.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(max(numel, 1), dtype=dtype, device=self.device)
+            self._ws[name] = t
+        return t[:numel]
+
+    # ------------------------------------------------------------ barriers
+    def _signals(self, ranks: range) -> list[int]:
+        return [self.heap.peer(r, 0) for r in ranks]
+
+    def _barrier(self, ranks: range, epoch: int) -> None:
+        if len(ranks) > 1:
+            ops.group_barrier(self._signals(ranks), self.rank - ranks.start, ranks.start, epoch)
+
+    def _next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
+
+    # ------------------------------------------------------------ one micro-batch
+    def local_buffers(self, sp: StepPlan, mb: RankMicroBatch):
+        """Views of this rank's output buffers for micro-batch `mb` (inside the heap)."""
+        hd = self.n_heads * self.head_dim
+        out = self.heap.view(sp.offsets["out_local"], (mb.n_local, self.n_heads, self.head_dim),
+                             torch.bfloat16)
+        dqkv = self.heap.view(sp.offsets["dqkv_local"], (mb.n_local, 3, self.n_heads, self.head_dim),
+                              torch.bfloat16)
+        del hd
+        return out, dqkv
+
+    def micro_batch_forward(self, sp: StepPlan, mb: RankMicroBatch, qkv_local: torch.Tensor):
+        """Eq. (2)-(4) forward on this rank.  qkv_local: [n_local, 3, H, D] bf16.
+
+        Returns (out_local view [n_local, H, D], saved) where saved feeds the backward.
+        """
+        self._barrier(range(self.world_size), self._next_epoch())  # regroup point
+        grp = mb.group
+        if grp is None:
+            for _ in range(2):
+                self._next_epoch()
+            return None, None
+        H, D = self.n_heads, self.head_dim
+        d, j, R = grp.degree, mb.j, grp.rows_per_rank
+        hs = H // d
+        ranks = grp.ranks
+        if qkv_local.shape[0] != mb.n_local:
+            raise ValueError(f"rank {self.rank} expects {mb.n_local} local rows, got {qkv_local.shape[0]}")
+        off = sp.offsets
+        recv = self.heap.view(off["qkv_recv"], (grp.padded_tokens, 3, hs, D), torch.bfloat16)
+        sent = float((d - 1) * R * hs * D * 2)  # NVLink bytes this rank sends per matrix
+        with self.timer.span("a2a", 3 * sent):
+            self._a2a_qkv(sp, mb, qkv_local, grp, R, hs)
+            self._barrier(ranks, self._next_epoch())
+        o_heads = self._workspace("o_heads", grp.padded_tokens * hs * D, torch.bfloat16).view(
+            grp.padded_tokens, hs, D)
+        with self.timer.span("attn_fwd", mb.fwd_flops):
+            o_heads, lse = ops.attn_fwd(recv[:, 0], recv[:, 1], recv[:, 2], mb.sched, self.scale,
+                                        out=o_heads)
+        out_local, _ = self.local_buffers(sp, mb)
+        with self.timer.span("a2a", sent):
+            ops.a2a("head2seq", o_heads.view(grp.padded_tokens, hs * D),
+                    [self.heap.peer(r, off["out_local"]) for r in ranks], degree=d, rank=j,
+                    rows_per_rank=R, n_mats=1, n_heads=H, head_dim=D, dst_stride=H * D,
+                    index=mb.unpack_table)
+            self._barrier(ranks, self._next_epoch())
+        return out_local, (recv, o_heads, lse)
+
+    def _a2a_qkv(self, sp, mb, qkv_local, grp, R, hs):
+        H, D, d, j = self.n_heads, self.head_dim, grp.degree, mb.j
+        off = sp.offsets
+        ops.a2a("seq2head", qkv_local.view(mb.n_local, -1) if mb.n_local else
+                qkv_local.reshape(0, 3 * H * D),
+                [self.heap.peer(r, off["qkv_recv"]) for r in grp.ranks], degree=d, rank=j,
+                rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * hs * D,
+                index=mb.pack_index)
+
+    def micro_batch_backward(self, sp: StepPlan, mb: RankMicroBatch, saved, dout_local: torch.Tensor):
+        """Backward of micro_batch_forward: dout_local [n_local, H, D] -> dqkv_local view."""
+        grp = mb.group
+        if grp is None:
+            for _ in range(2):
+                self._next_epoch()
+            return None
+        recv, o_heads, lse = saved
+        H, D = self.n_heads, self.head_dim
+        d, j, R = grp.degree, mb.j, grp.rows_per_rank
+        hs = H // d
+        ranks = grp.ranks
+        off = sp.offsets
+        do_recv = self.heap.view(off["do_recv"], (grp.padded_tokens, hs, D), torch.bfloat16)
+        sent = float((d - 1) * R * hs * D * 2)
+        with self.timer.span("a2a", sent):
+            ops.a2a("seq2head", dout_local.reshape(mb.n_local, H * D),
+                    [self.heap.peer(r, off["do_recv"]) for r in ranks], degree=d, rank=j,
+                    rows_per_rank=R, n_mats=1, n_heads=H, head_dim=D, dst_stride=hs * D,
+                    index=mb.pack_index)
+            self._barrier(ranks, self._next_epoch())
+        T = grp.padded_tokens
+        dqkv_heads = self._workspace("dqkv_heads", T * 3 * hs * D, torch.bfloat16).view(T, 3, hs, D)
+        dq_acc = self._workspace("dq_accum", T * hs * D, torch.float32)
+        delta = self._workspace("delta", hs * T, torch.float32)
+        with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
+            ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, do_recv, lse, mb.sched,
+                         self.scale, dq=dqkv_heads[:, 0], dk=dqkv_heads[:, 1],
+                         dv=dqkv_heads[:, 2], dq_accum=dq_acc, delta=delta)
+        _, dqkv_local = self.local_buffers(sp, mb)
+        with self.timer.span("a2a", 3 * sent):
+            ops.a2a("head2seq", dqkv_heads.view(T, 3 * hs * D),
+                    [self.heap.peer(r, off["dqkv_local"]) for r in ranks], degree=d, rank=j,
+                    rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * H * D,
+                    index=mb.unpack_table)
+            self._barrier(ranks, self._next_epoch())
+        return dqkv_local
+
+    def step(self, sp: StepPlan, qkv_locals: Sequence[torch.Tensor],
+             dout_locals: Sequence[torch.Tensor], sink=None):
+        """fwd+bwd of every micro-batch in plan order.  `sink(m, out, dqkv)` consumes the
+        outputs before the next micro-batch reuses the heap regions (e.g. a copy-out)."""
+        for m, mb in enumerate(sp.micro_batches):
+            out, saved = self.micro_batch_forward(sp, mb, qkv_locals[m])
+            dqkv = self.micro_batch_backward(sp, mb, saved, dout_locals[m])
+            if sink is not None:
+                sink(m, out, dqkv)

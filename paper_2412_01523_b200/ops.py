@@ -13,6 +13,7 @@ import numpy as np
 import torch
 
 from . import capi
+from .profiling import LAUNCHES
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
 
@@ -40,6 +41,7 @@ def pack_rows(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor) -> torc
     capi.check(lib.fsp_pack_rows(src.data_ptr(), src.stride(0) * src.element_size(),
                                  out.data_ptr(), out.stride(0) * out.element_size(),
                                  index.data_ptr(), out.shape[0], row_bytes, _stream()))
+    LAUNCHES[0] += 1 if out.shape[0] else 0
     return out
 
 
@@ -51,6 +53,7 @@ def unpack_rows(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor) -> to
     capi.check(lib.fsp_unpack_rows(src.data_ptr(), src.stride(0) * src.element_size(),
                                    out.data_ptr(), out.stride(0) * out.element_size(),
                                    index.data_ptr(), src.shape[0], row_bytes, _stream()))
+    LAUNCHES[0] += 1 if src.shape[0] else 0
     return out
 
 
@@ -66,9 +69,13 @@ class AttnSchedule:
     max_seqlen: int
 
     @staticmethod
-    def build(cu_seqlens_host, device) -> "AttnSchedule":
+    def build(cu_seqlens_host, device, total_rows: int | None = None) -> "AttnSchedule":
+        """`total_rows` >= cu[-1] lets the packed buffer carry trailing pad rows."""
         cu = np.ascontiguousarray(np.asarray(cu_seqlens_host, dtype=np.int32))
         n_seq = len(cu) - 1
+        rows = int(cu[-1]) if total_rows is None else int(total_rows)
+        if rows < int(cu[-1]):
+            raise ValueError("total_rows smaller than the packed sequences")
         lib = capi.load()
         cu_p = cu.ctypes.data_as(_i32p)
         tiles = []
@@ -83,7 +90,7 @@ class AttnSchedule:
             tiles.append(torch.from_numpy(buf[:n].copy()).to(device))
         lens = np.diff(cu)
         return AttnSchedule(torch.from_numpy(cu.copy()).to(device), tiles[0], tiles[1], n_seq,
-                            int(cu[-1]), int(lens.max()) if n_seq else 0)
+                            rows, int(lens.max()) if n_seq else 0)
 
 
 def _rows_view_ok(t: torch.Tensor, H: int, D: int) -> None:
@@ -110,23 +117,32 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
                         sched.cu_seqlens.data_ptr(), sched.fwd_tiles.data_ptr(),
                         sched.fwd_tiles.numel(), sched.n_seq, T, H, D, scale)
     capi.check(capi.load().fsp_attn_fwd(ctypes.byref(a), _stream()))
+    LAUNCHES[0] += 1 if sched.fwd_tiles.numel() else 0
     return o, lse
 
 
 def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | None = None,
-             dq=None, dk=None, dv=None):
-    """Varlen causal attention backward -> (dq, dk, dv), each [T, H, D] bf16."""
+             dq=None, dk=None, dv=None, dq_accum=None, delta=None):
+    """Varlen causal attention backward -> (dq, dk, dv), each [T, H, D] bf16.
+
+    dq_accum (fp32 [T, H, D]) and delta (fp32 [H, T]) are optional reusable workspaces.
+    """
     _require_cuda(q, k, v, o, dout, lse)
     T, H, D = q.shape
     for t in (q, k, v, o, dout):
         _rows_view_ok(t, H, D)
+    if T != sched.total_rows:
+        raise ValueError(f"q has {T} rows but the schedule covers {sched.total_rows}")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(D)
     dev = q.device
     dq = dq if dq is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
     dk = dk if dk is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
     dv = dv if dv is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
-    dq_acc = torch.empty((T, H, D), dtype=torch.float32, device=dev)
-    delta = torch.empty((H, T), dtype=torch.float32, device=dev)
+    dq_acc = dq_accum if dq_accum is not None else torch.empty((T, H, D), dtype=torch.float32,
+                                                               device=dev)
+    delta = delta if delta is not None else torch.empty((H, T), dtype=torch.float32, device=dev)
+    if dq_acc.numel() < T * H * D or delta.numel() < H * T:
+        raise ValueError("attention backward workspace too small")
     a = capi.FspAttnBwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(),
                         lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
                         q.stride(0), k.stride(0), v.stride(0), o.stride(0), dout.stride(0),
@@ -134,6 +150,7 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
                         delta.data_ptr(), sched.cu_seqlens.data_ptr(), sched.bwd_tiles.data_ptr(),
                         sched.bwd_tiles.numel(), sched.n_seq, T, H, D, scale)
     capi.check(capi.load().fsp_attn_bwd(ctypes.byref(a), _stream()))
+    LAUNCHES[0] += (2 if T else 0) + (1 if sched.bwd_tiles.numel() else 0)
     return dq, dk, dv
 
 
@@ -143,3 +160,41 @@ def selftest_umma(mode: int, a: torch.Tensor, b: torch.Tensor, k: int) -> torch.
     capi.check(capi.load().fsp_selftest_umma(mode, a.data_ptr(), b.data_ptr(), c.data_ptr(), k,
                                              _stream()))
     return c
+
+
+# ---------------------------------------------------------------- all-to-all
+def _ptr_array(ptrs) -> ctypes.Array:
+    arr = (ctypes.c_void_p * len(ptrs))()
+    for i, p in enumerate(ptrs):
+        arr[i] = int(p)
+    return arr
+
+
+def a2a(direction: str, src: torch.Tensor, peer_dst_ptrs, *, degree: int, rank: int,
+        rows_per_rank: int, n_mats: int, n_heads: int, head_dim: int, dst_stride: int,
+        index: torch.Tensor | None = None) -> None:
+    """One Ulysses exchange (Eq. 2 'seq2head' / Eq. 4 'head2seq') over peer pointers.
+
+    `src` is a row-major CUDA tensor whose dim-0 stride is the source row stride;
+    `peer_dst_ptrs[j]` is group member j's destination base (device address valid in
+    this process); `dst_stride` is the destination row stride in elements.
+    """
+    _require_cuda(src)
+    if index is not None:
+        _require_cuda(index)
+        if index.dtype != torch.int32:
+            raise ValueError("a2a index must be int32")
+    a = capi.FspA2A(degree, rank, rows_per_rank, n_mats, n_heads, head_dim, src.stride(0),
+                    dst_stride)
+    fn = capi.load().fsp_a2a_seq2head if direction == "seq2head" else capi.load().fsp_a2a_head2seq
+    if direction not in ("seq2head", "head2seq"):
+        raise ValueError(direction)
+    capi.check(fn(ctypes.byref(a), src.data_ptr(), _ptr_array(peer_dst_ptrs),
+                  None if index is None else index.data_ptr(), _stream()))
+    LAUNCHES[0] += 1 if rows_per_rank * n_mats else 0
+
+
+def group_barrier(signal_ptrs, rank: int, slot_base: int, epoch: int) -> None:
+    capi.check(capi.load().fsp_group_barrier(_ptr_array(signal_ptrs), len(signal_ptrs), rank,
+                                             slot_base, epoch & 0xFFFFFFFF, _stream()))
+    LAUNCHES[0] += 1 if len(signal_ptrs) > 1 else 0

@@ -1,0 +1,147 @@
+"""Generate the committed golden fixtures from the REFERENCE planner (run in the build
+container, where /root/reference is mounted; the GPU box only reads the outputs).
+
+    python tests/golden/make_golden.py
+
+Outputs (all small JSON/NPZ, committed):
+  c1_*.json       SURVEY.md Appendix B config-1 plans (two-tier flexsp, one-tier flexsp,
+                  static SP=2) — their sha256 prefixes are pinned in tests/test_golden.py
+  fig1_*.json     PAPER Fig. 1 scenario (pkg/tests/conftest.py:14-45): flexsp T*=3.0,
+                  degrees [32,8,8,8,8]; static SP=32
+  c2_n{N}_{flexsp,static}.json   C2 long-tail batch (gen_longtail(64, pareto 1.1, 32K),
+                  SURVEY.md §8d) planned for N = 1, 2, 4, 8 B200 with the B200
+                  attention-layer coefficients below — these are the bench's plans
+  rand_*.json     random small instances (N = 4, 8) for layout parity
+  attn_small.npz  attention golden vectors from oracle/attention_ref.py (fp32), checked
+                  against torch SDPA when generated
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+for cand in ("/root/reference/pkg/src", str(ROOT / "baseline" / "_ref")):
+    if os.path.isdir(cand) and cand not in sys.path:
+        sys.path.insert(0, cand)
+sys.path.insert(0, str(ROOT))
+
+from seqplan.baselines import plan_static  # noqa: E402
+from seqplan.domain import ClusterSpec, CostCoefficients, SequenceBatch  # noqa: E402
+from seqplan.simulator import gen_longtail  # noqa: E402
+from seqplan.workflow import SolveConfig, solve_batch  # noqa: E402
+
+# ---- C1
+C1_COEFFS = CostCoefficients(alpha1=3.584e-09, alpha2=9.437184e-06, beta1=1e-4, alpha3=8192,
+                             beta2=5e-05, m_token=17408, m_ms=1e6)
+C1_E = 143_606_336
+
+# ---- B200 attention-layer coefficients for the C2 GPT-7B shape (h=4096, H=32, D=128).
+# alpha1: measured round-1 kernel rates, fwd 2*D*H*s^2 FLOP at 718 TF/s + bwd 5*D*H*s^2 at
+#         428 TF/s (profiles/r01_*); alpha2: ~160 KB/token of HBM traffic at 6.5 TB/s;
+# alpha3: bytes crossing NVLink per token, fwd+bwd 2 x (3h + h) x 2 B;  bandwidth: d >= 2
+#         groups ride NVLink 5 at the measured 770 GB/s peer rate, d = 1 groups exchange
+#         nothing (the devices_per_node=1 tier trick).
+B200_ATTN_COEFFS = CostCoefficients(alpha1=5.93e-11, alpha2=2.5e-8, beta1=1e-4, alpha3=65536,
+                                    beta2=3e-5, m_token=2.0e5, m_ms=2e9)
+B200_E = 180e9
+
+
+def b200_cluster(n: int) -> ClusterSpec:
+    return ClusterSpec(n, 1, 1e15, 7.7e11, B200_E)
+
+
+def c2_batch() -> SequenceBatch:
+    return gen_longtail(64, ("pareto", 1.1, 1024), 32768, seed=0)[0]
+
+
+def c1_batch() -> SequenceBatch:
+    return gen_longtail(16, ("lognormal", 8.0, 1.4), 4096, seed=0)[0]
+
+
+def dump(name: str, obj) -> str:
+    text = json.dumps(obj, indent=2) + "\n"
+    (HERE / name).write_text(text)
+    return hashlib.sha256(text.encode()).hexdigest()[:16]
+
+
+def plan_doc(plan, batch, extra=None) -> dict:
+    d = plan.to_json_dict()
+    d["lengths"] = list(batch.lengths)
+    if extra:
+        d.update(extra)
+    return d
+
+
+def main():
+    meta = {}
+    # C1
+    b = c1_batch()
+    two = ClusterSpec(2, 1, 1e15, 5e10, C1_E)
+    one = ClusterSpec(2, 2, 5e10, 5e10, C1_E)
+    p = solve_batch(b, two, C1_COEFFS, SolveConfig(jobs=1))
+    meta["c1_flexsp_2tier"] = (p.to_json(), p.predicted_total_time)
+    dump("c1_flexsp_2tier.json", plan_doc(p, b))
+    p = solve_batch(b, one, C1_COEFFS, SolveConfig(jobs=1))
+    meta["c1_flexsp_1tier"] = (p.to_json(), p.predicted_total_time)
+    dump("c1_flexsp_1tier.json", plan_doc(p, b))
+    p = plan_static(b, two, C1_COEFFS, 2)
+    dump("c1_static2.json", plan_doc(p, b))
+    # Fig. 1
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import FIG1_CLUSTER, FIG1_COEFFS, FIG1_LENGTHS  # noqa: E402
+    fb = SequenceBatch(FIG1_LENGTHS, batch_id="fig1")
+    p = solve_batch(fb, FIG1_CLUSTER, FIG1_COEFFS, SolveConfig(jobs=1))
+    dump("fig1_flexsp.json", plan_doc(p, fb))
+    p = plan_static(fb, FIG1_CLUSTER, FIG1_COEFFS, 32)
+    dump("fig1_static32.json", plan_doc(p, fb))
+    # C2 at N = 1, 2, 4, 8
+    cb = c2_batch()
+    for n in (1, 2, 4, 8):
+        cl = b200_cluster(n)
+        p = solve_batch(cb, cl, B200_ATTN_COEFFS, SolveConfig(jobs=8, time_limit=60))
+        dump(f"c2_n{n}_flexsp.json", plan_doc(p, cb, {"coefficients": B200_ATTN_COEFFS.to_json_dict(),
+                                                      "cluster": cl.to_json_dict()}))
+        s = plan_static(cb, cl, B200_ATTN_COEFFS, n)
+        dump(f"c2_n{n}_static.json", plan_doc(s, cb, {"coefficients": B200_ATTN_COEFFS.to_json_dict(),
+                                                      "cluster": cl.to_json_dict()}))
+        print(f"C2 N={n}: flexsp {p.predicted_total_time:.5f}s "
+              f"{[sorted((g.degree for g in mb.selected_groups), reverse=True) for mb in p.micro_batches]}"
+              f" static {s.predicted_total_time:.5f}s")
+    # random small instances for layout parity
+    rng = np.random.default_rng(7)
+    for i, n in enumerate((4, 8, 4)):
+        lens = [int(x) for x in np.clip(rng.lognormal(6.0, 1.2, size=12), 1, 3000)]
+        rb = SequenceBatch(lens, batch_id=f"rand{i}")
+        coeffs = CostCoefficients(alpha1=1e-9, alpha2=1e-6, beta1=1e-4, alpha3=4096, beta2=1e-5,
+                                  m_token=2e4, m_ms=1e6)
+        cl = ClusterSpec(n, 1, 1e15, 2e10, 1e6 + 2e4 * 2500)
+        p = solve_batch(rb, cl, coeffs, SolveConfig(jobs=1))
+        dump(f"rand{i}_n{n}_flexsp.json", plan_doc(p, rb))
+    # attention golden vectors (oracle, cross-checked with SDPA)
+    import torch
+    from oracle.attention_ref import attention_bwd_ref, attention_fwd_ref, attention_sdpa_ref
+    lens = [37, 1, 130, 20]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    g = torch.Generator().manual_seed(2412)
+    q, k, v, do = (torch.randn(int(cu[-1]), 1, 64, generator=g).bfloat16() for _ in range(4))
+    o, lse = attention_fwd_ref(q, k, v, cu)
+    o2 = attention_sdpa_ref(q, k, v, cu)
+    assert torch.allclose(o, o2, atol=1e-5), (o - o2).abs().max()
+    dq, dk, dv = attention_bwd_ref(q, k, v, do, cu)
+    np.savez_compressed(HERE / "attn_small.npz", cu_seqlens=cu,
+                        q=q.view(torch.int16).numpy(), k=k.view(torch.int16).numpy(),
+                        v=v.view(torch.int16).numpy(), do=do.view(torch.int16).numpy(),
+                        o=o.numpy(), lse=lse.numpy(), dq=dq.numpy(), dk=dk.numpy(), dv=dv.numpy())
+    for key, (text, t) in meta.items():
+        print(key, hashlib.sha256(text.encode()).hexdigest()[:16], round(t, 6))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,85 @@
+"""C-ABI library checks that need no GPU: it builds, loads, exports every symbol the
+header declares, host-side argument validation maps to ValueError, and the LPT tile
+schedule (pure host code) matches a Python restatement."""
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2412_01523_b200 import _build, capi
+    if not capi.LIB_PATH.exists():
+        _build.build()
+    return capi.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    header = (ROOT / "include" / "flexsp_b200.h").read_text()
+    declared = set(re.findall(r"^\s*(?:int|int32_t|const char\*)\s+(fsp_\w+)\(", header, re.M))
+    assert declared, "no declarations parsed"
+    from paper_2412_01523_b200 import capi
+    assert declared == set(capi.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.fsp_abi_version() == 1
+
+
+def _schedule(lib, lens, rev):
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    p = cu.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    n = lib.fsp_attn_schedule(p, len(lens), rev, None, 0)
+    buf = np.zeros(max(n, 1), dtype=np.int32)
+    assert lib.fsp_attn_schedule(p, len(lens), rev, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n) == n
+    return [(int(x) >> 16, int(x) & 0xFFFF) for x in buf[:n]]
+
+
+@pytest.mark.parametrize("rev", [0, 1])
+def test_schedule_is_lpt_and_complete(lib, rev):
+    lens = [1, 128, 129, 0, 1000, 300, 4096]
+    tiles = _schedule(lib, lens, rev)
+    ntiles = [-(-s // 128) for s in lens]
+    expect = sorted((s, t) for s, n in enumerate(ntiles) for t in range(n))
+    assert sorted(tiles) == expect
+    cost = [(ntiles[s] - t) if rev else (t + 1) for s, t in tiles]
+    assert cost == sorted(cost, reverse=True)
+    # ties keep (sequence, tile) order -> deterministic
+    for a, b in zip(tiles, tiles[1:]):
+        ca = (ntiles[a[0]] - a[1]) if rev else a[1] + 1
+        cb = (ntiles[b[0]] - b[1]) if rev else b[1] + 1
+        if ca == cb:
+            assert a < b
+
+
+def test_invalid_arguments_raise_valueerror(lib):
+    from paper_2412_01523_b200 import capi
+    # row_bytes not a multiple of 16 -> rejected on the host before any CUDA call
+    rc = lib.fsp_pack_rows(16, 16, 16, 16, 16, 1, 10, None)
+    assert rc == capi.FSP_ERR_INVALID
+    with pytest.raises(ValueError):
+        capi.check(rc)
+    a = capi.FspAttnFwd()
+    a.head_dim = 96
+    a.n_heads = 1
+    rc = lib.fsp_attn_fwd(ctypes.byref(a), None)
+    assert rc == capi.FSP_ERR_INVALID
+    assert b"head_dim" in lib.fsp_last_error()
+    x = capi.FspA2A(3, 0, 1, 1, 4, 64, 256, 256)  # degree 3 is not a power of two
+    ptrs = (ctypes.c_void_p * 3)(16, 16, 16)
+    assert lib.fsp_a2a_seq2head(ctypes.byref(x), 16, ptrs, None, None) == capi.FSP_ERR_INVALID
+    cu = (ctypes.c_int32 * 3)(0, 5, 3)  # decreasing cu_seqlens
+    assert lib.fsp_attn_schedule(cu, 2, 0, None, 0) == capi.FSP_ERR_INVALID
+
+
+def test_device_ops_reject_cpu_tensors(lib):
+    from paper_2412_01523_b200 import ops
+    x = torch.zeros(4, 8, dtype=torch.bfloat16)
+    idx = torch.zeros(4, dtype=torch.int32)
+    with pytest.raises(ValueError, match="CUDA"):
+        ops.pack_rows(x, idx, x.clone())

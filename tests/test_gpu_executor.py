@@ -1,0 +1,147 @@
+"""GPU parity of the data-movement kernels (bit-exact) and of the full SP step.
+
+Multi-rank exchanges are emulated on one GPU by calling every member's kernel in turn
+with peer pointers aimed at per-member buffers on the same device (the kernels are
+rank-local and never wait on each other, so this is safe on a single GPU).
+"""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import layout_ref
+from oracle.attention_ref import attention_bwd_ref, attention_fwd_ref
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def _ops():
+    from paper_2412_01523_b200 import ops
+    return ops
+
+
+def test_pack_unpack_bit_exact():
+    ops = _ops()
+    g = torch.Generator().manual_seed(3)
+    for rows, cols in ((1000, 3 * 8 * 64), (37, 8), (5000, 24)):
+        src = torch.randint(-30000, 30000, (rows, cols), generator=g, dtype=torch.int16)
+        idx = torch.randperm(rows, generator=g)[: rows - 3].to(torch.int32)
+        idx = torch.cat([idx, torch.tensor([-1, -1], dtype=torch.int32)])
+        out = torch.empty((idx.numel(), cols), dtype=torch.int16, device="cuda")
+        ops.pack_rows(src.cuda(), idx.cuda(), out)
+        ref = torch.zeros_like(out.cpu())
+        live = idx >= 0
+        ref[live] = src[idx[live].long()]
+        assert torch.equal(out.cpu(), ref)
+        back = torch.zeros((rows, cols), dtype=torch.int16, device="cuda")
+        ops.unpack_rows(out, idx.cuda(), back)
+        ref2 = torch.zeros((rows, cols), dtype=torch.int16)
+        ref2[idx[live].long()] = src[idx[live].long()]
+        assert torch.equal(back.cpu(), ref2)
+
+
+@pytest.mark.parametrize("degree", [1, 2, 4, 8])
+def test_a2a_emulated_group_bit_exact(degree):
+    """seq2head (fused pack) and head2seq (fused unpack) for every member of a group,
+    against the numpy restatement of Eqs. (2)/(4) on the oracle's layout tables."""
+    ops = _ops()
+    from paper_2412_01523_b200.layout import build_microbatch_layout
+    H, D = 8, 64
+    lengths = [333, 1, 128, 77, 1000]
+    mb = {"selected_groups": [{"slot_id": 0, "degree": degree, "sequence_indices": [2, 0, 4, 1, 3]}]}
+    lay = build_microbatch_layout(mb, lengths, degree, n_heads=H)
+    grp = lay.groups[0]
+    T = sum(lengths)
+    g = torch.Generator().manual_seed(degree)
+    x = torch.randint(-30000, 30000, (T, 3, H, D), generator=g, dtype=torch.int16)  # loader order
+    R, hs = grp.rows_per_rank, H // degree
+    locals_ = [x[torch.from_numpy(grp.local_tokens(j))].contiguous().cuda() for j in range(degree)]
+    recv = [torch.full((grp.padded_tokens, 3, hs, D), 7, dtype=torch.int16, device="cuda")
+            for _ in range(degree)]
+    for j in range(degree):
+        idx = torch.from_numpy(grp.pack_index(j)).cuda()
+        src = locals_[j].view(locals_[j].shape[0], -1) if locals_[j].shape[0] else \
+            locals_[j].reshape(0, 3 * H * D)
+        ops.a2a("seq2head", src, [r.data_ptr() for r in recv], degree=degree, rank=j,
+                rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * hs * D, index=idx)
+    torch.cuda.synchronize()
+    perm = grp.perm
+    xp = np.zeros((grp.padded_tokens, 3, H, D), dtype=np.int16)
+    xp[perm >= 0] = x.numpy()[perm[perm >= 0]]
+    shards = [xp[j * R:(j + 1) * R] for j in range(degree)]
+    ref = layout_ref.ulysses_seq2head(shards, 3, H, D)
+    for j in range(degree):
+        np.testing.assert_array_equal(recv[j].cpu().numpy(), ref[j])
+    # head2seq back into loader-order local buffers: exact round trip
+    outs = [torch.zeros_like(l) for l in locals_]
+    table = torch.from_numpy(np.ascontiguousarray(grp.unpack_table().reshape(-1))).cuda()
+    for j in range(degree):
+        ops.a2a("head2seq", recv[j].view(grp.padded_tokens, -1), [o.data_ptr() for o in outs],
+                degree=degree, rank=j, rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D,
+                dst_stride=3 * H * D, index=table)
+    torch.cuda.synchronize()
+    for j in range(degree):
+        assert torch.equal(outs[j].cpu(), locals_[j].cpu())
+
+
+def _plan_n1(lengths, split):
+    mbs = []
+    for idx in split:
+        mbs.append({"selected_groups": [{"slot_id": 0, "degree": 1, "sequence_indices": idx}]})
+    return {"schema": 1, "strategy": "flexsp", "micro_batches": mbs}
+
+
+def test_executor_world1_matches_oracle():
+    """Full step through the executor (pack -> attn -> unpack, fwd+bwd) at N=1."""
+    from paper_2412_01523_b200.executor import FlexSPExecutor
+    H, D = 4, 128
+    lengths = [700, 1, 130, 2048, 64, 300]
+    plan = _plan_n1(lengths, [[3, 1, 5], [0, 2, 4]])
+    ex = FlexSPExecutor(1, 0, H, D, "cuda")
+    sp = ex.prepare(plan, lengths)
+    T = sum(lengths)
+    g = torch.Generator().manual_seed(1)
+    qkv = torch.randn(T, 3, H, D, generator=g).bfloat16()
+    dout = torch.randn(T, H, D, generator=g).bfloat16()
+    got_o = torch.zeros(T, H, D)
+    got_d = torch.zeros(T, 3, H, D)
+    ins, douts = [], []
+    for mb in sp.micro_batches:
+        tok = torch.from_numpy(mb.local_tokens)
+        ins.append(qkv[tok].cuda())
+        douts.append(dout[tok].cuda())
+
+    def sink(m, out, dqkv):
+        tok = torch.from_numpy(sp.micro_batches[m].local_tokens)
+        got_o[tok] = out.float().cpu()
+        got_d[tok] = dqkv.float().cpu()
+
+    ex.step(sp, ins, douts, sink=sink)
+    torch.cuda.synchronize()
+    offs = np.concatenate([[0], np.cumsum(lengths)])
+    cu = offs.astype(np.int32)  # loader order == per-sequence order for the oracle
+    o_ref, _ = attention_fwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], cu)
+    dq, dk, dv = attention_bwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], dout, cu)
+    diff = (got_o - o_ref).abs()
+    assert diff.max() <= 2e-2 and diff.mean() <= 2e-3
+    for i, ref in enumerate((dq, dk, dv)):
+        torch.testing.assert_close(got_d[:, i], ref, atol=5e-2, rtol=5e-2)
+
+
+def test_attention_golden_vectors():
+    """Kernel vs the committed oracle vectors (tests/golden/attn_small.npz, D=64)."""
+    ops = _ops()
+    z = np.load(GOLDEN / "attn_small.npz")
+    bf = lambda a: torch.from_numpy(a).view(torch.bfloat16).cuda()  # noqa: E731
+    q, k, v, do = bf(z["q"]), bf(z["k"]), bf(z["v"]), bf(z["do"])
+    sched = ops.AttnSchedule.build(z["cu_seqlens"], "cuda")
+    o, lse = ops.attn_fwd(q, k, v, sched)
+    dq, dk, dv = ops.attn_bwd(q, k, v, o, do, lse, sched)
+    torch.cuda.synchronize()
+    assert (o.float().cpu() - torch.from_numpy(z["o"])).abs().max() <= 2e-2
+    assert (lse.cpu() - torch.from_numpy(z["lse"])).abs().max() <= 1e-3 * 10
+    for got, key in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+        torch.testing.assert_close(got.float().cpu(), torch.from_numpy(z[key]), atol=5e-2, rtol=5e-2)

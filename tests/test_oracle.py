@@ -1,0 +1,92 @@
+"""CPU checks of the oracle itself (no GPU): attention restatement vs golden vectors and
+torch SDPA; Ulysses SP on gloo world_size=2 equals single-process attention; the
+numpy data-movement restatement agrees with the gloo exchange."""
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import layout_ref
+from oracle.attention_ref import attention_bwd_ref, attention_fwd_ref, attention_sdpa_ref
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def _golden():
+    z = np.load(GOLDEN / "attn_small.npz")
+    bf = lambda a: torch.from_numpy(a).view(torch.bfloat16)  # noqa: E731
+    return z, bf(z["q"]), bf(z["k"]), bf(z["v"]), bf(z["do"])
+
+
+def test_attention_oracle_matches_golden():
+    z, q, k, v, do = _golden()
+    cu = z["cu_seqlens"]
+    o, lse = attention_fwd_ref(q, k, v, cu)
+    np.testing.assert_allclose(o.numpy(), z["o"], atol=1e-6)
+    np.testing.assert_allclose(lse.numpy(), z["lse"], atol=1e-6)
+    dq, dk, dv = attention_bwd_ref(q, k, v, do, cu)
+    for got, key in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+        np.testing.assert_allclose(got.numpy(), z[key], atol=1e-5)
+
+
+def test_attention_oracle_matches_sdpa():
+    g = torch.Generator().manual_seed(5)
+    cu = np.array([0, 1, 70, 70, 200], dtype=np.int32)
+    q, k, v = (torch.randn(200, 3, 32, generator=g) for _ in range(3))
+    o, _ = attention_fwd_ref(q, k, v, cu)
+    torch.testing.assert_close(o, attention_sdpa_ref(q, k, v, cu), atol=1e-5, rtol=1e-5)
+
+
+def test_attention_oracle_no_cross_sequence_leak():
+    """Packing masks: changing sequence 1 must not change sequence 0."""
+    g = torch.Generator().manual_seed(6)
+    cu = np.array([0, 50, 120], dtype=np.int32)
+    q, k, v = (torch.randn(120, 2, 16, generator=g) for _ in range(3))
+    o1, _ = attention_fwd_ref(q, k, v, cu)
+    k2 = k.clone()
+    k2[60:] += 5.0
+    o2, _ = attention_fwd_ref(q, k2, v, cu)
+    torch.testing.assert_close(o1[:50], o2[:50])
+
+
+def _ulysses_worker(rank, world, port, q, cu, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.ulysses_ref import ulysses_attention
+    R = q.shape[0] // world
+    out = ulysses_attention(q[rank * R:(rank + 1) * R], cu)
+    torch.save(out, f"{out_path}.{rank}")
+    dist.destroy_process_group()
+
+
+def test_ulysses_gloo_world2_equals_single_process(tmp_path):
+    """Eq. (2)-(4) on two gloo ranks == attention without SP (SP is an identity)."""
+    g = torch.Generator().manual_seed(11)
+    lens = [97, 1, 200, 33]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(cu[-1])
+    Tp = -(-T // 2) * 2
+    qkv = torch.zeros(Tp, 3, 4, 16)
+    qkv[:T] = torch.randn(T, 3, 4, 16, generator=g)
+    port = 29500 + os.getpid() % 1000
+    mp.spawn(_ulysses_worker, args=(2, port, qkv, cu, str(tmp_path / "o")), nprocs=2)
+    got = torch.cat([torch.load(tmp_path / f"o.{r}") for r in range(2)])[:T]
+    ref, _ = attention_fwd_ref(qkv[:T, 0], qkv[:T, 1], qkv[:T, 2], cu)
+    torch.testing.assert_close(got, ref, atol=1e-5, rtol=1e-5)
+
+
+def test_numpy_exchange_restatement_roundtrip():
+    rng = np.random.default_rng(0)
+    d, R, M, H, D = 4, 3, 3, 8, 2
+    shards = [rng.standard_normal((R, M, H, D)) for _ in range(d)]
+    heads = layout_ref.ulysses_seq2head(shards, M, H, D)
+    assert heads[1].shape == (d * R, M, H // d, D)
+    np.testing.assert_array_equal(heads[2][R:2 * R, :, :, :], shards[1][:, :, 4:6, :])
+    back = layout_ref.ulysses_head2seq(heads, M, H, D)
+    for a, b in zip(back, shards):
+        np.testing.assert_array_equal(a, b)
