@@ -22,7 +22,7 @@
 namespace fsp {
 
 int make_head_tmap(CUtensorMap* m, const void* base, int64_t row_stride_elems, int n_heads,
-                   int head_dim, int rows);
+                   int head_dim, int rows, int box_rows);
 int check_attn_common(const void* q, const void* k, const void* v, int64_t qs, int64_t ks,
                       int64_t vs, const int32_t* cu, const int32_t* tiles, int32_t n_tiles,
                       int32_t n_seq, int32_t total_rows, int32_t n_heads, int32_t head_dim);
@@ -379,6 +379,303 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
   }
 }
 
+// ============================================================================ v2 (D = 128)
+// Same math as attn_bwd_kernel, restructured so the tensor core never idles on the
+// softmax-gradient warps: each 128-row query tile is processed as two 64-column
+// half-tiles u = 2*it + h whose S^T / dP^T live in separate TMEM stages, so
+//   MMA:     S/dP(u)  | grads(u-1) | S/dP(u+1) | grads(u) ...
+//   compute:          | P,dS(u)    | dQ(u-1)   | P,dS(u+1) ...
+// dQ is produced transposed (dQ^T = K^T dS^T, M = D lanes, N = 64 query columns) into the
+// stage's dP columns, so every TMEM stage is 64 columns:
+// TMEM: dK [0,128) dV [128,256) S0 [256,320) S1 [320,384) dP0|dQ0 [384,448) dP1|dQ1 [448,512)
+// 8 compute warps: two per TMEM lane quadrant, each owning 32 of the 64 columns.
+constexpr int kV2Compute = 8;
+constexpr int kV2Threads = 64 + 32 * kV2Compute;
+constexpr uint32_t kV2ColS = 256, kV2ColDP = 384;
+
+struct BwdSmemV2 {
+  static constexpr int kTileBytes = 128 * 128 * 2;
+  static constexpr int kHalfBytes = 64 * 128 * 2;     // one 64-row half of Q_i or dO_i
+  static constexpr int kSlots = 6;                    // 3 half tiles of (Q, dO) in flight
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + kTileBytes;
+  static constexpr int kRing = kV + kTileBytes;
+  static constexpr int kDS = kRing + kSlots * kHalfBytes;  // 2 stages x [128 kv][64 q] bf16
+  static constexpr int kStat = kDS + 2 * 16384;       // lse2[2][128], delta[2][128]
+  static constexpr int kBar = kStat + 4 * 128 * 4;
+  static constexpr int kBytes = kBar + 256;
+};
+
+__global__ void __launch_bounds__(kV2Threads, 1)
+    attn_bwd_kernel_v2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                       const BwdParams p) {
+  constexpr int D = 128;
+  using L = BwdSmemV2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  float* lse_s = reinterpret_cast<float*>(smem + L::kStat);  // [2][128]
+  float* delta_s = lse_s + 256;                              // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_kv = bars + 0;
+  uint64_t* ring_full = bars + 1;   // [6]
+  uint64_t* ring_empty = bars + 7;  // [6]
+  uint64_t* s_full = bars + 13;     // [2]
+  uint64_t* p_ready = bars + 15;    // [2]
+  uint64_t* dq_full = bars + 17;    // [2]
+  uint64_t* tm_free = bars + 19;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int head = blockIdx.x % p.n_heads;
+  const int tile = p.tiles[blockIdx.x / p.n_heads];
+  const int seq = tile >> 16;
+  const int kt = tile & 0xFFFF;
+  const int seq_start = p.cu_seqlens[seq];
+  const int seqlen = p.cu_seqlens[seq + 1] - seq_start;
+  const int kv0 = kt * kTile;
+  const int nq = (seqlen + kTile - 1) / kTile;
+  const int n_it = nq - kt;
+  const int n_u = 2 * n_it;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_kv, 1);
+    for (int i = 0; i < L::kSlots; ++i) {
+      mbar_init(ring_full + i, 1);
+      mbar_init(ring_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(p_ready + i, kV2Compute);
+      mbar_init(dq_full + i, 1);
+      mbar_init(tm_free + i, kV2Compute);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      tma_prefetch(&tm_do);
+      mbar_expect_tx(bar_kv, 2 * L::kTileBytes);
+      for (int b = 0; b < 2; ++b) {
+        tma_load_3d(smem + L::kK + b * 16384, &tm_k, bar_kv, b * 64, head, seq_start + kv0);
+        tma_load_3d(smem + L::kV + b * 16384, &tm_v, bar_kv, b * 64, head, seq_start + kv0);
+      }
+      // items 2u / 2u+1 = Q / dO rows of half tile u (64 rows each)
+      for (int item = 0; item < 2 * n_u; ++item) {
+        const int slot = item % L::kSlots;
+        const uint32_t ph = (item / L::kSlots) & 1;
+        const int row = seq_start + kv0 + (item >> 1) * 64;
+        mbar_wait(ring_empty + slot, ph ^ 1);
+        mbar_expect_tx(ring_full + slot, L::kHalfBytes);
+        const CUtensorMap* map = (item & 1) ? &tm_do : &tm_q;
+        for (int b = 0; b < 2; ++b)
+          tma_load_3d(smem + L::kRing + slot * L::kHalfBytes + b * 8192, map, ring_full + slot,
+                      b * 64, head, row);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // Q/dO half tiles: K-major boxes of [64 rows][64 d] (8 KB, SBO 1024); MN-major view for
+    // dK/dV: d chunks 8 KB apart (LBO), 16 query rows = 2048 B per K step.
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idesc_dvdk = make_idesc_bf16(128, D, false, true);
+      constexpr uint32_t idesc_dqt = make_idesc_bf16(128, 64, true, true);
+      const uint32_t k_base = smem_u32(smem + L::kK);
+      const uint32_t v_base = smem_u32(smem + L::kV);
+      const uint32_t ring_base = smem_u32(smem + L::kRing);
+      const uint32_t ds_base = smem_u32(smem + L::kDS);
+      mbar_wait(bar_kv, 0);
+      auto grads = [&](int u) {
+        const int it = u >> 1, h = u & 1;
+        const int sq = (2 * u) % L::kSlots, sd = (2 * u + 1) % L::kSlots;
+        const uint32_t q_base = ring_base + sq * L::kHalfBytes;
+        const uint32_t do_base = ring_base + sd * L::kHalfBytes;
+        const uint32_t dsb = ds_base + h * 16384;
+        mbar_wait(p_ready + h, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO_h      (K = 64 query rows)
+          mma_ts(tmem + kColDV, tmem + kV2ColS + h * 64 + kk * 8,
+                 make_sdesc_sw128(do_base + kk * 2048, 8192, 1024), idesc_dvdk,
+                 (u > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q_h
+          mma_ss(tmem + kColDK, make_sdesc_sw128(dsb + kk * 32, 16, 1024),
+                 make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
+                 (u > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 kv rows)
+          mma_ss(tmem + kV2ColDP + h * 64, make_sdesc_sw128(k_base + kk * 2048, 16384, 1024),
+                 make_sdesc_sw128(dsb + kk * 2048, 16384, 1024), idesc_dqt, kk > 0);
+        tc_commit(dq_full + h);
+        tc_commit(ring_empty + sq);
+        tc_commit(ring_empty + sd);
+      };
+      for (int u = 0; u < n_u; ++u) {
+        const int it = u >> 1, h = u & 1;
+        const int sq = (2 * u) % L::kSlots, sd = (2 * u + 1) % L::kSlots;
+        const uint32_t q_base = ring_base + sq * L::kHalfBytes;
+        const uint32_t do_base = ring_base + sd * L::kHalfBytes;
+        if (u >= 2) mbar_wait(tm_free + h, (it - 1) & 1);
+        mbar_wait(ring_full + sq, ((2 * u) / L::kSlots) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          mma_ss(tmem + kV2ColS + h * 64,
+                 make_sdesc_sw128(k_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                 make_sdesc_sw128(q_base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_s,
+                 kk > 0);
+        }
+        mbar_wait(ring_full + sd, ((2 * u + 1) / L::kSlots) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          mma_ss(tmem + kV2ColDP + h * 64,
+                 make_sdesc_sw128(v_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                 make_sdesc_sw128(do_base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_s,
+                 kk > 0);
+        }
+        tc_commit(s_full + h);
+        if (u >= 1) grads(u - 1);
+      }
+      if (n_u > 0) grads(n_u - 1);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ compute warps
+    const uint32_t cw = warp - 2;              // 0..7
+    const uint32_t quad = warp & 3;            // TMEM lane quadrant
+    const uint32_t ch = cw >> 2;               // which 32 of the 64 columns
+    const int r = quad * 32 + lane;            // kv row (S^T, dP^T) / d index (dQ^T)
+    const uint32_t lane_addr = (quad * 32u) << 16;
+    const int kv_pos = kv0 + r;
+    const float sl2 = p.scale_log2;
+    const int ctid = cw * 32 + lane;           // 0..255
+    auto readout = [&](int u) {                // dQ^T(u): lane r = d, columns = query rows
+      const int it = u >> 1, h = u & 1;
+      mbar_wait(dq_full + h, it & 1);
+      tc_fence_after();
+      uint32_t qr[32];
+      tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, qr);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tm_free + h);
+      const int qb = (kt + it) * kTile + h * 64 + ch * 32;  // first query row of this slice
+      float* base = p.dq_accum + ((int64_t)(seq_start + qb) * p.n_heads + head) * D + r;
+      const int64_t rs = (int64_t)p.n_heads * D;
+      const int nvalid = seqlen - qb;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid)
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + i * rs), "f"(__uint_as_float(qr[i]))
+                       : "memory");
+    };
+    for (int it = 0; it < n_it; ++it) {
+      const int q0 = (kt + it) * kTile;
+      const int buf = it & 1;
+      {
+        const int t = ctid & 127;
+        const bool valid = q0 + t < seqlen;
+        const int64_t gi = (int64_t)head * p.total_rows + seq_start + q0 + t;
+        if (ctid < 128)
+          lse_s[buf * 128 + t] = valid ? p.lse[gi] * kLog2e : INFINITY;
+        else
+          delta_s[buf * 128 + t] = valid ? p.delta[gi] : 0.f;
+      }
+      named_bar_sync(1, 32 * kV2Compute);
+      for (int h = 0; h < 2; ++h) {
+        const int u = 2 * it + h;
+        const int c0 = h * 64 + ch * 32;  // query column offset inside the 128-row tile
+        const float* ls = lse_s + buf * 128 + c0;
+        const float* dl = delta_s + buf * 128 + c0;
+        mbar_wait(s_full + h, it & 1);
+        tc_fence_after();
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, sr);
+        tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, dr);
+        tmem_ld_wait();
+        // both column halves of every lane must be read before P^T overwrites S
+        named_bar_sync(2 + h, 32 * kV2Compute);
+        const bool diag = (it == 0);
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p0 = ex2(fmaf(__uint_as_float(sr[i]), sl2, -ls[i]));
+          float p1 = ex2(fmaf(__uint_as_float(sr[i + 1]), sl2, -ls[i + 1]));
+          if (diag) {  // causal on the diagonal tile: query column c0+i >= kv row r
+            if (c0 + i < r) p0 = 0.f;
+            if (c0 + i + 1 < r) p1 = 0.f;
+          }
+          pk[i / 2] = pack_bf16(p0, p1);
+          dk[i / 2] = pack_bf16(p0 * (__uint_as_float(dr[i]) - dl[i]),
+                                p1 * (__uint_as_float(dr[i + 1]) - dl[i + 1]));
+        }
+        tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, pk);
+        // dS^T row r, query columns [ch*32, ch*32+32) of this half: 16-byte chunks 4ch+v
+        uint8_t* row = smem + L::kDS + h * 16384 + r * 128;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int chunk = (4 * (int)ch + v) ^ (r & 7);
+          *reinterpret_cast<uint4*>(row + chunk * 16) =
+              make_uint4(dk[4 * v], dk[4 * v + 1], dk[4 * v + 2], dk[4 * v + 3]);
+        }
+        tmem_st_wait();
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_ready + h);
+        if (u >= 1) readout(u - 1);
+      }
+    }
+    if (n_u > 0) readout(n_u - 1);
+    // ---- epilogue: this thread writes D/2 columns of dK (scaled) and dV for kv row r
+    {
+      const bool kvalid = kv_pos < seqlen;
+      __nv_bfloat16* dk_row = p.dk + (int64_t)(seq_start + kv_pos) * p.dk_stride + (int64_t)head * D;
+      __nv_bfloat16* dv_row = p.dv + (int64_t)(seq_start + kv_pos) * p.dv_stride + (int64_t)head * D;
+#pragma unroll
+      for (int c = ch * 64; c < ch * 64 + 64; c += 32) {
+        uint32_t a[32], b[32];
+        tmem_ld32(tmem + lane_addr + kColDK + c, a);
+        tmem_ld32(tmem + lane_addr + kColDV + c, b);
+        tmem_ld_wait();
+        if (!kvalid) continue;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 vk, vv;
+          vk.x = pack_bf16(__uint_as_float(a[i]) * p.scale, __uint_as_float(a[i + 1]) * p.scale);
+          vk.y = pack_bf16(__uint_as_float(a[i + 2]) * p.scale, __uint_as_float(a[i + 3]) * p.scale);
+          vk.z = pack_bf16(__uint_as_float(a[i + 4]) * p.scale, __uint_as_float(a[i + 5]) * p.scale);
+          vk.w = pack_bf16(__uint_as_float(a[i + 6]) * p.scale, __uint_as_float(a[i + 7]) * p.scale);
+          vv.x = pack_bf16(__uint_as_float(b[i]), __uint_as_float(b[i + 1]));
+          vv.y = pack_bf16(__uint_as_float(b[i + 2]), __uint_as_float(b[i + 3]));
+          vv.z = pack_bf16(__uint_as_float(b[i + 4]), __uint_as_float(b[i + 5]));
+          vv.w = pack_bf16(__uint_as_float(b[i + 6]), __uint_as_float(b[i + 7]));
+          *reinterpret_cast<uint4*>(dk_row + c + i) = vk;
+          *reinterpret_cast<uint4*>(dv_row + c + i) = vv;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free<512>(tmem);
+}
+
 template <int D>
 int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
   const int T = a->total_rows, H = a->n_heads;
@@ -394,10 +691,12 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
   if (a->n_tiles > 0) {
     CUtensorMap tq, tk, tv, tdo;
     int rc;
-    if ((rc = make_head_tmap(&tq, a->q, a->q_stride, H, D, T))) return rc;
-    if ((rc = make_head_tmap(&tk, a->k, a->k_stride, H, D, T))) return rc;
-    if ((rc = make_head_tmap(&tv, a->v, a->v_stride, H, D, T))) return rc;
-    if ((rc = make_head_tmap(&tdo, a->dout, a->do_stride, H, D, T))) return rc;
+    // v2 (D = 128) streams Q / dO in 64-row half tiles; v1 in 128-row tiles
+    const int qrows = D == 128 ? 64 : 128;
+    if ((rc = make_head_tmap(&tq, a->q, a->q_stride, H, D, T, qrows))) return rc;
+    if ((rc = make_head_tmap(&tk, a->k, a->k_stride, H, D, T, 128))) return rc;
+    if ((rc = make_head_tmap(&tv, a->v, a->v_stride, H, D, T, 128))) return rc;
+    if ((rc = make_head_tmap(&tdo, a->dout, a->do_stride, H, D, T, qrows))) return rc;
     BwdParams p;
     p.dk = reinterpret_cast<__nv_bfloat16*>(a->dk);
     p.dv = reinterpret_cast<__nv_bfloat16*>(a->dv);
@@ -412,11 +711,17 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     p.n_heads = H;
     p.scale = a->softmax_scale;
     p.scale_log2 = a->softmax_scale * kLog2e;
-    const int smem = BwdSmem<D>::kBytes + 1024;
-    FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t grid = (int64_t)a->n_tiles * H;
     FSP_CHECK_ARG(grid < (1ll << 31), "grid too large");
-    attn_bwd_kernel<D><<<(unsigned)grid, kBwdThreads, smem, stream>>>(tq, tk, tv, tdo, p);
+    if (D == 128) {
+      const int smem = BwdSmemV2::kBytes + 1024;
+      FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attn_bwd_kernel_v2<<<(unsigned)grid, kV2Threads, smem, stream>>>(tq, tk, tv, tdo, p);
+    } else {
+      const int smem = BwdSmem<D>::kBytes + 1024;
+      FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attn_bwd_kernel<D><<<(unsigned)grid, kBwdThreads, smem, stream>>>(tq, tk, tv, tdo, p);
+    }
     FSP_LAUNCH_CHECK();
   }
   {

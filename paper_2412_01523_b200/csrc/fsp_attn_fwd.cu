@@ -277,12 +277,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 }  // namespace
 
 // Tensor map over one bf16 operand of a token-major packed buffer:
-// dims {D, H, rows}, strides {D*2 (head), row_stride*2 (token)}, box {64, 1, 128}.
+// dims {D, H, rows}, strides {D*2 (head), row_stride*2 (token)}, box {64, 1, box_rows}.
 int make_head_tmap(CUtensorMap* m, const void* base, int64_t row_stride_elems, int n_heads,
-                   int head_dim, int rows) {
+                   int head_dim, int rows, int box_rows) {
   uint64_t dims[3] = {(uint64_t)head_dim, (uint64_t)n_heads, (uint64_t)rows};
   uint64_t strides[2] = {(uint64_t)head_dim * 2, (uint64_t)row_stride_elems * 2};
-  uint32_t box[3] = {64, 1, 128};
+  uint32_t box[3] = {64, 1, (uint32_t)box_rows};
   return encode_tmap_bf16(m, base, 3, dims, strides, box);
 }
 
@@ -290,9 +290,9 @@ template <int D>
 static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   CUtensorMap tq, tk, tv;
   int rc;
-  if ((rc = make_head_tmap(&tq, a->q, a->q_stride, a->n_heads, D, a->total_rows))) return rc;
-  if ((rc = make_head_tmap(&tk, a->k, a->k_stride, a->n_heads, D, a->total_rows))) return rc;
-  if ((rc = make_head_tmap(&tv, a->v, a->v_stride, a->n_heads, D, a->total_rows))) return rc;
+  if ((rc = make_head_tmap(&tq, a->q, a->q_stride, a->n_heads, D, a->total_rows, 128))) return rc;
+  if ((rc = make_head_tmap(&tk, a->k, a->k_stride, a->n_heads, D, a->total_rows, 128))) return rc;
+  if ((rc = make_head_tmap(&tv, a->v, a->v_stride, a->n_heads, D, a->total_rows, 128))) return rc;
   FwdParams p;
   p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
   p.lse = a->lse;
