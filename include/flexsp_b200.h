@@ -147,13 +147,14 @@ typedef struct FspAttnBwd {
   float softmax_scale;
 } FspAttnBwd;
 
-/* Longest-processing-time-first schedule of 128-row tiles over the sequences.
- * Writes up to `capacity` int32 entries (seq << 16 | tile) to tiles_host (may be NULL
- * to query) and returns the tile count (negative on error).  Causal cost of a tile
- * grows with its index, so tiles are ordered by decreasing work; `reverse_causal`
- * selects the backward (kv-tile) cost model. */
-int32_t fsp_attn_schedule(const int32_t* cu_seqlens_host, int32_t n_seq, int32_t reverse_causal,
-                          int32_t* tiles_host, int32_t capacity);
+/* CTA schedule over (sequence, head, 128-row tile): writes n entries of two int32
+ * {seq << 16 | tile, head} to tiles_host (2*capacity words; NULL to query) and returns n
+ * (negative on error).  Sequences longest first; within a sequence one head at a time,
+ * heaviest tile first (causal cost: forward tile t = t+1 kv tiles; backward kv tile t =
+ * n_tiles - t, selected by `reverse_causal`), so the resident CTAs share one head's
+ * operands in L2.  n_tiles in FspAttnFwd/FspAttnBwd is this n. */
+int32_t fsp_attn_schedule(const int32_t* cu_seqlens_host, int32_t n_seq, int32_t n_heads,
+                          int32_t reverse_causal, int32_t* tiles_host, int32_t capacity);
 int fsp_attn_fwd(const FspAttnFwd* a, void* stream);
 int fsp_attn_bwd(const FspAttnBwd* a, void* stream);
 

@@ -81,7 +81,7 @@ def load() -> ctypes.CDLL:
     lib.fsp_a2a_seq2head.argtypes = [ctypes.POINTER(FspA2A), c_vp, ctypes.POINTER(c_vp), c_vp, c_vp]
     lib.fsp_a2a_head2seq.argtypes = [ctypes.POINTER(FspA2A), c_vp, ctypes.POINTER(c_vp), c_vp, c_vp]
     lib.fsp_group_barrier.argtypes = [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, ctypes.c_uint32, c_vp]
-    lib.fsp_attn_schedule.argtypes = [ctypes.POINTER(c_i32), c_i32, c_i32, ctypes.POINTER(c_i32), c_i32]
+    lib.fsp_attn_schedule.argtypes = [ctypes.POINTER(c_i32), c_i32, c_i32, c_i32, ctypes.POINTER(c_i32), c_i32]
     lib.fsp_attn_schedule.restype = c_i32
     lib.fsp_attn_fwd.argtypes = [ctypes.POINTER(FspAttnFwd), c_vp]
     lib.fsp_attn_bwd.argtypes = [ctypes.POINTER(FspAttnBwd), c_vp]

@@ -90,8 +90,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int head = blockIdx.x % p.n_heads;
-  const int tile = p.tiles[blockIdx.x / p.n_heads];
+  const int tile = p.tiles[2 * blockIdx.x];
+  const int head = p.tiles[2 * blockIdx.x + 1];
   const int seq = tile >> 16;
   const int kt = tile & 0xFFFF;
   const int seq_start = p.cu_seqlens[seq];
@@ -428,8 +428,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int head = blockIdx.x % p.n_heads;
-  const int tile = p.tiles[blockIdx.x / p.n_heads];
+  const int tile = p.tiles[2 * blockIdx.x];
+  const int head = p.tiles[2 * blockIdx.x + 1];
   const int seq = tile >> 16;
   const int kt = tile & 0xFFFF;
   const int seq_start = p.cu_seqlens[seq];
@@ -711,8 +711,7 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     p.n_heads = H;
     p.scale = a->softmax_scale;
     p.scale_log2 = a->softmax_scale * kLog2e;
-    const int64_t grid = (int64_t)a->n_tiles * H;
-    FSP_CHECK_ARG(grid < (1ll << 31), "grid too large");
+    const int64_t grid = a->n_tiles;
     if (D == 128) {
       const int smem = BwdSmemV2::kBytes + 1024;
       FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -60,16 +60,25 @@ def unpack_rows(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor) -> to
 # ---------------------------------------------------------------- attention schedule
 @dataclass
 class AttnSchedule:
-    """cu_seqlens of one packed group plus the LPT tile orders for fwd and bwd."""
+    """cu_seqlens of one packed group plus the CTA orders (fsp_attn_schedule) for fwd/bwd."""
     cu_seqlens: torch.Tensor      # int32 [n_seq+1] device
-    fwd_tiles: torch.Tensor       # int32 device
-    bwd_tiles: torch.Tensor       # int32 device
+    fwd_tiles: torch.Tensor       # int32 [2 * n_fwd] device: {seq<<16 | tile, head}
+    bwd_tiles: torch.Tensor       # int32 [2 * n_bwd] device
     n_seq: int
+    n_heads: int
     total_rows: int
     max_seqlen: int
 
+    @property
+    def n_fwd(self) -> int:
+        return self.fwd_tiles.numel() // 2
+
+    @property
+    def n_bwd(self) -> int:
+        return self.bwd_tiles.numel() // 2
+
     @staticmethod
-    def build(cu_seqlens_host, device, total_rows: int | None = None) -> "AttnSchedule":
+    def build(cu_seqlens_host, device, n_heads: int, total_rows: int | None = None) -> "AttnSchedule":
         """`total_rows` >= cu[-1] lets the packed buffer carry trailing pad rows."""
         cu = np.ascontiguousarray(np.asarray(cu_seqlens_host, dtype=np.int32))
         n_seq = len(cu) - 1
@@ -80,17 +89,17 @@ class AttnSchedule:
         cu_p = cu.ctypes.data_as(_i32p)
         tiles = []
         for rev in (0, 1):
-            n = lib.fsp_attn_schedule(cu_p, n_seq, rev, None, 0)
+            n = lib.fsp_attn_schedule(cu_p, n_seq, n_heads, rev, None, 0)
             if n < 0:
                 capi.check(n)
-            buf = np.zeros(max(n, 1), dtype=np.int32)
-            got = lib.fsp_attn_schedule(cu_p, n_seq, rev, buf.ctypes.data_as(_i32p), n)
+            buf = np.zeros(max(2 * n, 2), dtype=np.int32)
+            got = lib.fsp_attn_schedule(cu_p, n_seq, n_heads, rev, buf.ctypes.data_as(_i32p), n)
             if got < 0:
                 capi.check(got)
-            tiles.append(torch.from_numpy(buf[:n].copy()).to(device))
+            tiles.append(torch.from_numpy(buf[:2 * n].copy()).to(device))
         lens = np.diff(cu)
         return AttnSchedule(torch.from_numpy(cu.copy()).to(device), tiles[0], tiles[1], n_seq,
-                            rows, int(lens.max()) if n_seq else 0)
+                            n_heads, rows, int(lens.max()) if n_seq else 0)
 
 
 def _rows_view_ok(t: torch.Tensor, H: int, D: int) -> None:
@@ -107,17 +116,18 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
     T, H, D = q.shape
     for t in (q, k, v):
         _rows_view_ok(t, H, D)
-    if T != sched.total_rows:
-        raise ValueError(f"q has {T} rows but cu_seqlens covers {sched.total_rows}")
+    if T != sched.total_rows or H != sched.n_heads:
+        raise ValueError(f"q is [{T}, {H}, .] but the schedule covers {sched.total_rows} rows, "
+                         f"{sched.n_heads} heads")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(D)
     o = out if out is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=q.device)
     lse = torch.empty((H, T), dtype=torch.float32, device=q.device)
     a = capi.FspAttnFwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
                         q.stride(0), k.stride(0), v.stride(0), o.stride(0),
                         sched.cu_seqlens.data_ptr(), sched.fwd_tiles.data_ptr(),
-                        sched.fwd_tiles.numel(), sched.n_seq, T, H, D, scale)
+                        sched.n_fwd, sched.n_seq, T, H, D, scale)
     capi.check(capi.load().fsp_attn_fwd(ctypes.byref(a), _stream()))
-    LAUNCHES[0] += 1 if sched.fwd_tiles.numel() else 0
+    LAUNCHES[0] += 1 if sched.n_fwd else 0
     return o, lse
 
 
@@ -131,8 +141,9 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
     T, H, D = q.shape
     for t in (q, k, v, o, dout):
         _rows_view_ok(t, H, D)
-    if T != sched.total_rows:
-        raise ValueError(f"q has {T} rows but the schedule covers {sched.total_rows}")
+    if T != sched.total_rows or H != sched.n_heads:
+        raise ValueError(f"q is [{T}, {H}, .] but the schedule covers {sched.total_rows} rows, "
+                         f"{sched.n_heads} heads")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(D)
     dev = q.device
     dq = dq if dq is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
@@ -148,9 +159,9 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
                         q.stride(0), k.stride(0), v.stride(0), o.stride(0), dout.stride(0),
                         dq.stride(0), dk.stride(0), dv.stride(0), dq_acc.data_ptr(),
                         delta.data_ptr(), sched.cu_seqlens.data_ptr(), sched.bwd_tiles.data_ptr(),
-                        sched.bwd_tiles.numel(), sched.n_seq, T, H, D, scale)
+                        sched.n_bwd, sched.n_seq, T, H, D, scale)
     capi.check(capi.load().fsp_attn_bwd(ctypes.byref(a), _stream()))
-    LAUNCHES[0] += (2 if T else 0) + (1 if sched.bwd_tiles.numel() else 0)
+    LAUNCHES[0] += (2 if T else 0) + (1 if sched.n_bwd else 0)
     return dq, dk, dv
 
 

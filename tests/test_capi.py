@@ -31,30 +31,34 @@ def test_exports_every_declared_symbol(lib):
     assert lib.fsp_abi_version() == 1
 
 
-def _schedule(lib, lens, rev):
+def _schedule(lib, lens, rev, heads=1):
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     p = cu.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    n = lib.fsp_attn_schedule(p, len(lens), rev, None, 0)
-    buf = np.zeros(max(n, 1), dtype=np.int32)
-    assert lib.fsp_attn_schedule(p, len(lens), rev, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n) == n
-    return [(int(x) >> 16, int(x) & 0xFFFF) for x in buf[:n]]
+    n = lib.fsp_attn_schedule(p, len(lens), heads, rev, None, 0)
+    buf = np.zeros(max(2 * n, 2), dtype=np.int32)
+    ptr = buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    assert lib.fsp_attn_schedule(p, len(lens), heads, rev, ptr, n) == n
+    return [(int(buf[2 * i]) >> 16, int(buf[2 * i]) & 0xFFFF, int(buf[2 * i + 1])) for i in range(n)]
 
 
 @pytest.mark.parametrize("rev", [0, 1])
-def test_schedule_is_lpt_and_complete(lib, rev):
+def test_schedule_complete_and_ordered(lib, rev):
     lens = [1, 128, 129, 0, 1000, 300, 4096]
-    tiles = _schedule(lib, lens, rev)
+    heads = 3
+    tiles = _schedule(lib, lens, rev, heads)
     ntiles = [-(-s // 128) for s in lens]
-    expect = sorted((s, t) for s, n in enumerate(ntiles) for t in range(n))
+    expect = sorted((s, t, h) for s, n in enumerate(ntiles) for t in range(n) for h in range(heads))
     assert sorted(tiles) == expect
-    cost = [(ntiles[s] - t) if rev else (t + 1) for s, t in tiles]
-    assert cost == sorted(cost, reverse=True)
-    # ties keep (sequence, tile) order -> deterministic
-    for a, b in zip(tiles, tiles[1:]):
-        ca = (ntiles[a[0]] - a[1]) if rev else a[1] + 1
-        cb = (ntiles[b[0]] - b[1]) if rev else b[1] + 1
-        if ca == cb:
-            assert a < b
+    # sequences longest first; inside a sequence head-major, heaviest tile first
+    seq_order = [s for s, _, _ in tiles]
+    firsts = list(dict.fromkeys(seq_order))
+    assert [ntiles[s] for s in firsts] == sorted((ntiles[s] for s in firsts), reverse=True)
+    for s in firsts:
+        block = [(t, h) for ss, t, h in tiles if ss == s]
+        assert [h for _, h in block] == sorted(h for _, h in block)
+        for h in range(heads):
+            costs = [(ntiles[s] - t) if rev else (t + 1) for t, hh in block if hh == h]
+            assert costs == sorted(costs, reverse=True)
 
 
 def test_invalid_arguments_raise_valueerror(lib):
@@ -74,7 +78,7 @@ def test_invalid_arguments_raise_valueerror(lib):
     ptrs = (ctypes.c_void_p * 3)(16, 16, 16)
     assert lib.fsp_a2a_seq2head(ctypes.byref(x), 16, ptrs, None, None) == capi.FSP_ERR_INVALID
     cu = (ctypes.c_int32 * 3)(0, 5, 3)  # decreasing cu_seqlens
-    assert lib.fsp_attn_schedule(cu, 2, 0, None, 0) == capi.FSP_ERR_INVALID
+    assert lib.fsp_attn_schedule(cu, 2, 1, 0, None, 0) == capi.FSP_ERR_INVALID
 
 
 def test_device_ops_reject_cpu_tensors(lib):
