@@ -29,46 +29,63 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return r;
 }
 
-// Index space (j, i, m, v): destination peer j outermost so a contiguous range of
-// vectors lands in one peer buffer as one long run; i = shard row, m = matrix (q/k/v),
-// v = 16-byte vector inside the (H/d)*D head slice.
+// One warp moves one (row i, matrix m, peer j) chunk = the (H/d)*D*2-byte head slice of
+// one row (1 KB at C2/d=8): index math once per chunk, 32 lanes x 16-byte vectors with
+// kUnroll loads in flight per lane.  Peer j is the fastest-varying chunk coordinate so the
+// local copy (j == rank) and the NVLink writes to all peers proceed concurrently, and the
+// source row is read sequentially.
+constexpr int kUnroll = 4;
+
 template <bool kSeq2Head>
 __global__ void __launch_bounds__(kThreads) a2a_kernel(const uint8_t* __restrict__ src,
                                                        PeerPtrs dst, const int32_t* __restrict__ index,
                                                        FspA2A a) {
   const int d = a.degree;
-  const int64_t slice_bytes = (int64_t)(a.n_heads / d) * a.head_dim * 2;
-  const uint32_t vpc = (uint32_t)(slice_bytes / 16);
-  const int64_t per_peer = (int64_t)a.rows_per_rank * a.n_mats * vpc;
-  const int64_t total = per_peer * d;
+  const int slice_bytes = (a.n_heads / d) * a.head_dim * 2;
+  const int vpc = slice_bytes >> 4;
+  const uint32_t n_chunks = (uint32_t)a.rows_per_rank * (uint32_t)a.n_mats * (uint32_t)d;
   const int64_t src_stride = a.src_stride * 2, dst_stride = a.dst_stride * 2;
   const int64_t full_row = (int64_t)a.n_heads * a.head_dim * 2;  // bytes of all heads of one mat
-  for (int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * kThreads) {
-    const int j = (int)(g / per_peer);
-    int64_t rem = g - (int64_t)j * per_peer;
-    const uint32_t v = (uint32_t)(rem % vpc);
-    rem /= vpc;
-    const int m = (int)(rem % a.n_mats);
-    const int i = (int)(rem / a.n_mats);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (kThreads / 32);
+  for (uint32_t c = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); c < n_chunks; c += warps) {
+    const uint32_t j = c % d;
+    const uint32_t rm = c / d;
+    const uint32_t m = rm % a.n_mats;
+    const uint32_t i = rm / a.n_mats;
+    const int4* sp;
+    int4* dp;
+    bool zero = false;
     if (kSeq2Head) {
       // local shard row i (all heads) -> peer j row (rank*R + i), head slice j
-      const int32_t srow = index ? index[i] : i;
-      int4 val = make_int4(0, 0, 0, 0);
-      if (srow >= 0)
-        val = ld_stream(reinterpret_cast<const int4*>(src + (int64_t)srow * src_stride +
-                                                      m * full_row + j * slice_bytes) + v);
+      const int32_t srow = index ? index[i] : (int32_t)i;
+      zero = srow < 0;
+      sp = reinterpret_cast<const int4*>(src + (int64_t)(zero ? 0 : srow) * src_stride +
+                                         m * full_row + (int64_t)j * slice_bytes);
       const int64_t drow = (int64_t)a.rank * a.rows_per_rank + i;
-      *(reinterpret_cast<int4*>(dst.p[j] + drow * dst_stride + m * slice_bytes) + v) = val;
+      dp = reinterpret_cast<int4*>(dst.p[j] + drow * dst_stride + (int64_t)m * slice_bytes);
     } else {
       // local row (j*R + i), own head slice -> peer j shard row i at head slice `rank`
       const int64_t srow = (int64_t)j * a.rows_per_rank + i;
-      const int32_t drow = index ? index[(int64_t)j * a.rows_per_rank + i] : i;
-      if (drow < 0) continue;
-      const int4 val =
-          ld_stream(reinterpret_cast<const int4*>(src + srow * src_stride + m * slice_bytes) + v);
-      *(reinterpret_cast<int4*>(dst.p[j] + (int64_t)drow * dst_stride + m * full_row +
-                                a.rank * slice_bytes) + v) = val;
+      const int32_t drow = index ? index[(int64_t)j * a.rows_per_rank + i] : (int32_t)i;
+      if (drow < 0) continue;  // pad row: dropped (warp-uniform)
+      sp = reinterpret_cast<const int4*>(src + srow * src_stride + (int64_t)m * slice_bytes);
+      dp = reinterpret_cast<int4*>(dst.p[j] + (int64_t)drow * dst_stride + m * full_row +
+                                   (int64_t)a.rank * slice_bytes);
+    }
+    for (int v0 = 0; v0 < vpc; v0 += 32 * kUnroll) {
+      int4 val[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int v = v0 + u * 32 + lane;
+        val[u] = make_int4(0, 0, 0, 0);
+        if (v < vpc && !zero) val[u] = ld_stream(sp + v);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < vpc) dp[v] = val[u];
+      }
     }
   }
   // make the peer stores visible system-wide before the group barrier publishes
@@ -122,10 +139,10 @@ int launch_a2a(const FspA2A* a, const void* src, void* const* peer_dst, const in
     FSP_CHECK_ARG(a->src_stride >= slice && a->dst_stride >= full, "strides too small");
   PeerPtrs pp{};
   for (int j = 0; j < a->degree; ++j) pp.p[j] = reinterpret_cast<uint8_t*>(peer_dst[j]);
-  const int64_t vecs = (int64_t)a->rows_per_rank * a->n_mats * a->degree *
-                       ((int64_t)(a->n_heads / a->degree) * a->head_dim * 2 / 16);
-  if (vecs == 0) return FSP_OK;
-  int64_t blocks = (vecs + kThreads - 1) / kThreads;
+  const int64_t chunks = (int64_t)a->rows_per_rank * a->n_mats * a->degree;
+  FSP_CHECK_ARG(chunks < (1ll << 32), "exchange too large");
+  if (chunks == 0) return FSP_OK;
+  int64_t blocks = (chunks + kThreads / 32 - 1) / (kThreads / 32);
   if (blocks > 148 * 8) blocks = 148 * 8;
   a2a_kernel<kSeq2Head><<<(unsigned)blocks, kThreads, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<const uint8_t*>(src), pp, index, *a);
