@@ -135,7 +135,7 @@ typedef struct FspAttnBwd {
   void* dk;
   void* dv;
   int64_t q_stride, k_stride, v_stride, o_stride, do_stride, dq_stride, dk_stride, dv_stride;
-  float* dq_accum;    /* workspace fp32 [total_rows, n_heads, head_dim] */
+  float* dq_accum;    /* workspace fp32 [n_heads, total_rows, head_dim] */
   float* delta;       /* workspace fp32 [n_heads, total_rows] */
   const int32_t* d_cu_seqlens;
   const int32_t* d_tiles; /* kv-tile schedule (same format as forward) */

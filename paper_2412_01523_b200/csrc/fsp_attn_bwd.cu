@@ -12,10 +12,12 @@
 //               dV  += P^T dO_i           (TS: A = P^T in TMEM, B = dO_i MN-major)
 //               dK  += dS^T Q_i           (SS: A = dS^T K-major, B = Q_i MN-major)
 //               dQ_i = dS K               (SS: A = dS MN-major (same smem), B = K MN-major)
-//             dQ_i is read out of TMEM and added to dq_accum with vector reductions.
-//   3. post:  dq = bf16(dq_accum * scale)
+//             dQ_i is read out of TMEM and added to dq_accum ([H, T, D] fp32) with reductions.
+//   3. post:  dq[t, h] = bf16(dq_accum[h, t] * scale)
 // TMEM (512 cols): dK [0,128) dV [128,256) S^T|P^T [256,384) dP^T|dQ [384,512).
 // smem: K, V (resident), a 3-slot ring of 32 KB tiles streaming Q_i / dO_i, dS (32 KB).
+#include <type_traits>
+
 #include "fsp_host.h"
 #include "fsp_ptx.cuh"
 
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(dq_full, it & 1);
       tc_fence_after();
       const bool qvalid = q0 + r < seqlen;
-      float* dq_row = p.dq_accum + ((int64_t)(seq_start + q0 + r) * p.n_heads + head) * D;
+      float* dq_row = p.dq_accum + ((int64_t)head * p.total_rows + seq_start + q0 + r) * D;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t qr[32];
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 1) tmem_free<512>(tmem);
 }
 
-// delta[h, t] = <O[t,h,:], dO[t,h,:]> in fp32; dq_accum[t,h,:] = 0.  One warp per (t, h).
+// delta[h, t] = <O[t,h,:], dO[t,h,:]> in fp32; dq_accum[h,t,:] = 0.  One warp per (t, h).
 template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(
     const __nv_bfloat16* __restrict__ o, int64_t o_stride, const __nv_bfloat16* __restrict__ dout,
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
     if (lane == 0) delta[(int64_t)h * total_rows + t] = acc;
-    float* dq = dq_accum + (t * n_heads + h) * D + lane * kPer;
+    float* dq = dq_accum + ((int64_t)h * total_rows + t) * D + lane * kPer;
     if (kPer == 4)
       *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
     else
@@ -357,40 +359,47 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(
   }
 }
 
-// dq[t, h*D + i] = bf16(dq_accum[t, h, i] * scale); 8 elements per thread.
+// dq[t, h*D + i] = bf16(dq_accum[h, t, i] * scale); 8 elements per thread.
+template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restrict__ dq_accum,
                                                             __nv_bfloat16* __restrict__ dq,
                                                             int64_t dq_stride, int total_rows,
-                                                            int row_elems, float scale) {
-  const int64_t per_row = row_elems / 8;
-  const int64_t n = (int64_t)total_rows * per_row;
+                                                            int n_heads, float scale) {
+  constexpr int kPerRow = D / 8;
+  const int64_t n = (int64_t)total_rows * n_heads * kPerRow;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
        g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = g / per_row;
-    const int64_t c = (g - t * per_row) * 8;
-    const float4 a = *reinterpret_cast<const float4*>(dq_accum + t * row_elems + c);
-    const float4 b = *reinterpret_cast<const float4*>(dq_accum + t * row_elems + c + 4);
+    const int c = (int)(g % kPerRow) * 8;
+    const int64_t th = g / kPerRow;
+    const int h = (int)(th % n_heads);
+    const int64_t t = th / n_heads;
+    const float* src = dq_accum + ((int64_t)h * total_rows + t) * D + c;
+    const float4 a = *reinterpret_cast<const float4*>(src);
+    const float4 b = *reinterpret_cast<const float4*>(src + 4);
     uint4 v;
     v.x = pack_bf16(a.x * scale, a.y * scale);
     v.y = pack_bf16(a.z * scale, a.w * scale);
     v.z = pack_bf16(b.x * scale, b.y * scale);
     v.w = pack_bf16(b.z * scale, b.w * scale);
-    *reinterpret_cast<uint4*>(dq + t * dq_stride + c) = v;
+    *reinterpret_cast<uint4*>(dq + t * dq_stride + (int64_t)h * D + c) = v;
   }
 }
 
 // ============================================================================ v2 (D = 128)
-// Same math as attn_bwd_kernel, restructured so the tensor core never idles on the
-// softmax-gradient warps: each 128-row query tile is processed as two 64-column
-// half-tiles u = 2*it + h whose S^T / dP^T live in separate TMEM stages, so
-//   MMA:     S/dP(u)  | grads(u-1) | S/dP(u+1) | grads(u) ...
-//   compute:          | P,dS(u)    | dQ(u-1)   | P,dS(u+1) ...
-// dQ is produced transposed (dQ^T = K^T dS^T, M = D lanes, N = 64 query columns) into the
-// stage's dP columns, so every TMEM stage is 64 columns:
+// Same math as attn_bwd_kernel, restructured so the tensor core does not wait on the
+// gradient warps: each 128-row query tile is processed as two 64-column half tiles
+// u = 2*it + h whose S^T / dP^T live in separate TMEM stages, so the MMA issue order is
+//   S/dP(u+1) | grads(u) | S/dP(u+2) | grads(u+1) ...
+// while 8 compute warps turn S/dP(u) into P^T (TMEM) and dS^T (smem) and 4 reduction warps
+// drain dQ^T(u-1) from TMEM into the fp32 accumulator in parallel.  dQ is produced
+// transposed (dQ^T = K^T dS^T, M = D lanes, N = 64 query columns) into the stage's dP
+// columns, so every TMEM stage is 64 columns:
 // TMEM: dK [0,128) dV [128,256) S0 [256,320) S1 [320,384) dP0|dQ0 [384,448) dP1|dQ1 [448,512)
-// 8 compute warps: two per TMEM lane quadrant, each owning 32 of the 64 columns.
+// Warps: 0 TMA, 1 MMA, 2..9 compute (two per TMEM lane quadrant, 32 of the 64 columns
+// each), 10..13 dQ reduction (one per quadrant, all 64 columns).
 constexpr int kV2Compute = 8;
-constexpr int kV2Threads = 64 + 32 * kV2Compute;
+constexpr int kV2Reduce = 4;
+constexpr int kV2Threads = 64 + 32 * (kV2Compute + kV2Reduce);
 constexpr uint32_t kV2ColS = 256, kV2ColDP = 384;
 
 struct BwdSmemV2 {
@@ -449,7 +458,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       mbar_init(s_full + i, 1);
       mbar_init(p_ready + i, kV2Compute);
       mbar_init(dq_full + i, 1);
-      mbar_init(tm_free + i, kV2Compute);
+      mbar_init(tm_free + i, kV2Reduce);
     }
     fence_mbar_init();
   }
@@ -516,6 +525,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
           mma_ss(tmem + kColDK, make_sdesc_sw128(dsb + kk * 32, 16, 1024),
                  make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
                  (u > 0 || kk > 0) ? 1u : 0u);
+        if (u >= 2) mbar_wait(tm_free + h, ((u >> 1) - 1) & 1);  // dQ^T(u-2) drained
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 kv rows)
           mma_ss(tmem + kV2ColDP + h * 64, make_sdesc_sw128(k_base + kk * 2048, 16384, 1024),
@@ -525,11 +536,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         tc_commit(ring_empty + sd);
       };
       for (int u = 0; u < n_u; ++u) {
-        const int it = u >> 1, h = u & 1;
+        const int h = u & 1;
         const int sq = (2 * u) % L::kSlots, sd = (2 * u + 1) % L::kSlots;
         const uint32_t q_base = ring_base + sq * L::kHalfBytes;
         const uint32_t do_base = ring_base + sd * L::kHalfBytes;
-        if (u >= 2) mbar_wait(tm_free + h, (it - 1) & 1);
+        // S^T(u) overwrites P^T(u-2), read by dV of grads(u-2) (issued earlier, in order);
+        // dP^T(u) overwrites dQ^T(u-2): wait until the reduction warps drained it.
         mbar_wait(ring_full + sq, ((2 * u) / L::kSlots) & 1);
         tc_fence_after();
 #pragma unroll
@@ -539,6 +551,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                  make_sdesc_sw128(q_base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_s,
                  kk > 0);
         }
+        if (u >= 2) mbar_wait(tm_free + h, ((u >> 1) - 1) & 1);
         mbar_wait(ring_full + sd, ((2 * u + 1) / L::kSlots) & 1);
         tc_fence_after();
 #pragma unroll
@@ -554,95 +567,83 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       if (n_u > 0) grads(n_u - 1);
     }
     __syncwarp();
-  } else {
+  } else if (warp < 2 + kV2Compute) {
     // ------------------------------------------------------------ compute warps
     const uint32_t cw = warp - 2;              // 0..7
     const uint32_t quad = warp & 3;            // TMEM lane quadrant
     const uint32_t ch = cw >> 2;               // which 32 of the 64 columns
-    const int r = quad * 32 + lane;            // kv row (S^T, dP^T) / d index (dQ^T)
+    const int r = quad * 32 + lane;            // kv row of S^T / dP^T
     const uint32_t lane_addr = (quad * 32u) << 16;
     const int kv_pos = kv0 + r;
     const float sl2 = p.scale_log2;
     const int ctid = cw * 32 + lane;           // 0..255
-    auto readout = [&](int u) {                // dQ^T(u): lane r = d, columns = query rows
-      const int it = u >> 1, h = u & 1;
-      mbar_wait(dq_full + h, it & 1);
+    // statistics of query tile `it`: thread ctid < 128 owns lse row ctid, others delta
+    auto load_stat = [&](int it) -> float {
+      const int t = ctid & 127;
+      const int q0 = (kt + it) * kTile;
+      const bool valid = q0 + t < seqlen;
+      const int64_t gi = (int64_t)head * p.total_rows + seq_start + q0 + t;
+      if (ctid < 128) return valid ? p.lse[gi] * kLog2e : INFINITY;
+      return valid ? p.delta[gi] : 0.f;
+    };
+    auto half = [&](auto diag_c, int it, int h) {
+      constexpr bool kDiag = decltype(diag_c)::value;
+      const int buf = it & 1;
+      const int c0 = h * 64 + ch * 32;  // query column offset inside the 128-row tile
+      const float* ls = lse_s + buf * 128 + c0;
+      const float* dl = delta_s + buf * 128 + c0;
+      mbar_wait(s_full + h, it & 1);
       tc_fence_after();
-      uint32_t qr[32];
-      tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, qr);
+      uint32_t sr[32], dr[32];
+      tmem_ld32(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, sr);
+      tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, dr);
       tmem_ld_wait();
+      // both column halves of every lane must be read before P^T overwrites S
+      named_bar_sync(2 + h, 32 * kV2Compute);
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float p0 = ex2(fmaf(__uint_as_float(sr[i]), sl2, -ls[i]));
+        float p1 = ex2(fmaf(__uint_as_float(sr[i + 1]), sl2, -ls[i + 1]));
+        if (kDiag) {  // causal on the diagonal tile: query column c0+i >= kv row r
+          if (c0 + i < r) p0 = 0.f;
+          if (c0 + i + 1 < r) p1 = 0.f;
+        }
+        pk[i / 2] = pack_bf16(p0, p1);
+        dk[i / 2] = pack_bf16(p0 * (__uint_as_float(dr[i]) - dl[i]),
+                              p1 * (__uint_as_float(dr[i + 1]) - dl[i + 1]));
+      }
+      tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, pk);
+      // dS^T row r, query columns [ch*32, ch*32+32) of this half: 16-byte chunks 4ch+v
+      uint8_t* row = smem + L::kDS + h * 16384 + r * 128;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int chunk = (4 * (int)ch + v) ^ (r & 7);
+        *reinterpret_cast<uint4*>(row + chunk * 16) =
+            make_uint4(dk[4 * v], dk[4 * v + 1], dk[4 * v + 2], dk[4 * v + 3]);
+      }
+      tmem_st_wait();
+      fence_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tm_free + h);
-      const int qb = (kt + it) * kTile + h * 64 + ch * 32;  // first query row of this slice
-      float* base = p.dq_accum + ((int64_t)(seq_start + qb) * p.n_heads + head) * D + r;
-      const int64_t rs = (int64_t)p.n_heads * D;
-      const int nvalid = seqlen - qb;
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (i < nvalid)
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + i * rs), "f"(__uint_as_float(qr[i]))
-                       : "memory");
+      if (lane == 0) mbar_arrive(p_ready + h);
     };
+    float stat = n_it > 0 ? load_stat(0) : 0.f;
     for (int it = 0; it < n_it; ++it) {
-      const int q0 = (kt + it) * kTile;
-      const int buf = it & 1;
-      {
-        const int t = ctid & 127;
-        const bool valid = q0 + t < seqlen;
-        const int64_t gi = (int64_t)head * p.total_rows + seq_start + q0 + t;
-        if (ctid < 128)
-          lse_s[buf * 128 + t] = valid ? p.lse[gi] * kLog2e : INFINITY;
-        else
-          delta_s[buf * 128 + t] = valid ? p.delta[gi] : 0.f;
-      }
+      (ctid < 128 ? lse_s : delta_s)[(it & 1) * 128 + (ctid & 127)] = stat;
+      if (it + 1 < n_it) stat = load_stat(it + 1);  // latency hidden behind this tile
       named_bar_sync(1, 32 * kV2Compute);
-      for (int h = 0; h < 2; ++h) {
-        const int u = 2 * it + h;
-        const int c0 = h * 64 + ch * 32;  // query column offset inside the 128-row tile
-        const float* ls = lse_s + buf * 128 + c0;
-        const float* dl = delta_s + buf * 128 + c0;
-        mbar_wait(s_full + h, it & 1);
-        tc_fence_after();
-        uint32_t sr[32], dr[32];
-        tmem_ld32(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, sr);
-        tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, dr);
-        tmem_ld_wait();
-        // both column halves of every lane must be read before P^T overwrites S
-        named_bar_sync(2 + h, 32 * kV2Compute);
-        const bool diag = (it == 0);
-        uint32_t pk[16], dk[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float p0 = ex2(fmaf(__uint_as_float(sr[i]), sl2, -ls[i]));
-          float p1 = ex2(fmaf(__uint_as_float(sr[i + 1]), sl2, -ls[i + 1]));
-          if (diag) {  // causal on the diagonal tile: query column c0+i >= kv row r
-            if (c0 + i < r) p0 = 0.f;
-            if (c0 + i + 1 < r) p1 = 0.f;
-          }
-          pk[i / 2] = pack_bf16(p0, p1);
-          dk[i / 2] = pack_bf16(p0 * (__uint_as_float(dr[i]) - dl[i]),
-                                p1 * (__uint_as_float(dr[i + 1]) - dl[i + 1]));
-        }
-        tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, pk);
-        // dS^T row r, query columns [ch*32, ch*32+32) of this half: 16-byte chunks 4ch+v
-        uint8_t* row = smem + L::kDS + h * 16384 + r * 128;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int chunk = (4 * (int)ch + v) ^ (r & 7);
-          *reinterpret_cast<uint4*>(row + chunk * 16) =
-              make_uint4(dk[4 * v], dk[4 * v + 1], dk[4 * v + 2], dk[4 * v + 3]);
-        }
-        tmem_st_wait();
-        fence_async_smem();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_ready + h);
-        if (u >= 1) readout(u - 1);
+      if (it == 0) {
+        half(std::true_type{}, it, 0);
+        half(std::true_type{}, it, 1);
+      } else {
+        half(std::false_type{}, it, 0);
+        half(std::false_type{}, it, 1);
       }
     }
-    if (n_u > 0) readout(n_u - 1);
     // ---- epilogue: this thread writes D/2 columns of dK (scaled) and dV for kv row r
+    if (n_u > 0) mbar_wait(dq_full + ((n_u - 1) & 1), ((n_u - 1) >> 1) & 1);  // all MMAs done
+    tc_fence_after();
     {
       const bool kvalid = kv_pos < seqlen;
       __nv_bfloat16* dk_row = p.dk + (int64_t)(seq_start + kv_pos) * p.dk_stride + (int64_t)head * D;
@@ -668,6 +669,44 @@ __global__ void __launch_bounds__(kV2Threads, 1)
           *reinterpret_cast<uint4*>(dk_row + c + i) = vk;
           *reinterpret_cast<uint4*>(dv_row + c + i) = vv;
         }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ dQ reduction warps
+    // dQ^T(u) in TMEM: lane = d, columns = the half tile's 64 query rows.  dq_accum is
+    // [H, T, D] fp32 so a warp's 32 lanes add 128 contiguous bytes per query row and the
+    // row stride (D*4 = 512 B) folds into the instruction's immediate offset.
+    const uint32_t quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_addr = (quad * 32u) << 16;
+    float* head_base = p.dq_accum + ((int64_t)head * p.total_rows + seq_start) * D + r;
+    for (int u = 0; u < n_u; ++u) {
+      const int it = u >> 1, h = u & 1;
+      mbar_wait(dq_full + h, it & 1);
+      tc_fence_after();
+      uint32_t qr[64];
+      tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64, *reinterpret_cast<uint32_t(*)[32]>(qr));
+      tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + 32,
+                *reinterpret_cast<uint32_t(*)[32]>(qr + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tm_free + h);
+      const int qb = (kt + it) * kTile + h * 64;  // first query row of this half (in sequence)
+      float* base = head_base + (int64_t)qb * D;
+      const int nvalid = seqlen - qb;
+      if (nvalid >= 64) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + i * D), "f"(__uint_as_float(qr[i]))
+                       : "memory");
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i < nvalid)
+            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + i * D),
+                         "f"(__uint_as_float(qr[i]))
+                         : "memory");
       }
     }
   }
@@ -728,8 +767,8 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (n > 0) {
-      attn_bwd_post_kernel<<<(unsigned)blocks, 256, 0, stream>>>(
-          a->dq_accum, reinterpret_cast<__nv_bfloat16*>(a->dq), a->dq_stride, T, H * D,
+      attn_bwd_post_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(
+          a->dq_accum, reinterpret_cast<__nv_bfloat16*>(a->dq), a->dq_stride, T, H,
           a->softmax_scale);
       FSP_LAUNCH_CHECK();
     }
