@@ -147,14 +147,17 @@ typedef struct FspAttnBwd {
   float softmax_scale;
 } FspAttnBwd;
 
-/* CTA schedule over (sequence, head, 128-row tile): writes n entries of two int32
- * {seq << 16 | tile, head} to tiles_host (2*capacity words; NULL to query) and returns n
- * (negative on error).  Sequences longest first; within a sequence one head at a time,
- * heaviest tile first (causal cost: forward tile t = t+1 kv tiles; backward kv tile t =
- * n_tiles - t, selected by `reverse_causal`), so the resident CTAs share one head's
- * operands in L2.  n_tiles in FspAttnFwd/FspAttnBwd is this n. */
+/* CTA schedule: writes n entries of two int32 {seq << 16 | unit, head} to tiles_host
+ * (2*capacity words; NULL to query) and returns n (negative on error).  kind
+ * FSP_SCHED_FWD: units are query tiles (128 rows; 256-row tile pairs when head_dim is
+ * 128, matching fsp_attn_fwd's kernel); FSP_SCHED_BWD: 128-row kv tiles.  Sequences
+ * longest first; within a sequence one head at a time, heaviest unit first (causal cost:
+ * forward unit t grows with t, backward kv tile t costs n_tiles - t), so the resident
+ * CTAs share one head's operands in L2.  n_tiles in FspAttnFwd/FspAttnBwd is this n. */
+#define FSP_SCHED_FWD 0
+#define FSP_SCHED_BWD 1
 int32_t fsp_attn_schedule(const int32_t* cu_seqlens_host, int32_t n_seq, int32_t n_heads,
-                          int32_t reverse_causal, int32_t* tiles_host, int32_t capacity);
+                          int32_t head_dim, int32_t kind, int32_t* tiles_host, int32_t capacity);
 int fsp_attn_fwd(const FspAttnFwd* a, void* stream);
 int fsp_attn_bwd(const FspAttnBwd* a, void* stream);
 

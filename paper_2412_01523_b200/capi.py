@@ -17,6 +17,8 @@ FSP_OK = 0
 FSP_ERR_INVALID = -1
 FSP_ERR_CUDA = -2
 FSP_ERR_UNSUPPORTED = -3
+FSP_SCHED_FWD = 0
+FSP_SCHED_BWD = 1
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -81,7 +83,8 @@ def load() -> ctypes.CDLL:
     lib.fsp_a2a_seq2head.argtypes = [ctypes.POINTER(FspA2A), c_vp, ctypes.POINTER(c_vp), c_vp, c_vp]
     lib.fsp_a2a_head2seq.argtypes = [ctypes.POINTER(FspA2A), c_vp, ctypes.POINTER(c_vp), c_vp, c_vp]
     lib.fsp_group_barrier.argtypes = [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, ctypes.c_uint32, c_vp]
-    lib.fsp_attn_schedule.argtypes = [ctypes.POINTER(c_i32), c_i32, c_i32, c_i32, ctypes.POINTER(c_i32), c_i32]
+    lib.fsp_attn_schedule.argtypes = [ctypes.POINTER(c_i32), c_i32, c_i32, c_i32, c_i32,
+                                      ctypes.POINTER(c_i32), c_i32]
     lib.fsp_attn_schedule.restype = c_i32
     lib.fsp_attn_fwd.argtypes = [ctypes.POINTER(FspAttnFwd), c_vp]
     lib.fsp_attn_bwd.argtypes = [ctypes.POINTER(FspAttnBwd), c_vp]

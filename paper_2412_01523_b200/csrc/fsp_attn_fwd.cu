@@ -276,6 +276,297 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 1) tmem_free<512>(tmem);
 }
 
+// ============================================================================ paired (D = 128)
+// One CTA = two consecutive 128-row query tiles A, B (256 rows) of one sequence x head
+// sharing every K_j / V_j load.  Two softmax warpgroups (one per tile) alternate with
+// the tensor core:
+//   MMA:  S_A(0) S_B(0) | PV_A(0) S_A(1) PV_B(0) S_B(1) | PV_A(1) S_A(2) ...
+// so QK^T / PV of one tile run while the other tile's softmax executes.  P_X is written
+// as bf16 over the first 64 columns of S_X (the S_X(j+1) MMA is issued after PV_X(j) and
+// tcgen05 MMAs execute in issue order).  s_full_X(j) is committed after PV_X(j-1), so a
+// softmax warpgroup may rescale O_X in place when it sees S_X(j).
+// Rescaling is lazy: the exponent base m only moves when the running max grows by more
+// than 8 (factor 256), which keeps P <= 256 and makes O rescales rare.
+// A quarter of the exponentials run as a degree-3 polynomial on the FMA pipe (the
+// 16/clk/SM MUFU.EX2 rate would otherwise equal the tensor-core time per tile).
+// TMEM: S_A|P_A [0,128) S_B|P_B [128,256) O_A [256,384) O_B [384,512).
+constexpr int kF2Threads = 64 + 256;
+
+struct Fwd2Smem {
+  static constexpr int kTileBytes = 128 * 128 * 2;
+  static constexpr int kQA = 0;
+  static constexpr int kQB = kTileBytes;
+  static constexpr int kK = 2 * kTileBytes;  // 2 stages
+  static constexpr int kV = 4 * kTileBytes;  // 2 stages
+  static constexpr int kBar = 6 * kTileBytes;
+  static constexpr int kBytes = kBar + 256;
+};
+
+// 2^x on the FMA pipe (x <= 0, finite): round-to-nearest split via the 1.5*2^23 magic
+// number, minimax cubic for 2^f on [-0.5, 0.5] (max rel. error 7.5e-5), exponent add.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float y = x + 12582912.f;
+  const float xi = y - 12582912.f;
+  const float f = x - xi;
+  float pf = fmaf(0.05517025f, f, 0.2426079f);
+  pf = fmaf(pf, f, 0.69326093f);
+  pf = fmaf(pf, f, 0.99992828f);
+  return __int_as_float(__float_as_int(pf) + (__float_as_int(y) << 23));
+}
+
+__global__ void __launch_bounds__(kF2Threads, 1)
+    attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+  constexpr int D = 128;
+  using L = Fwd2Smem;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_q = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2] per tile
+  uint64_t* p_full = bars + 11;  // [2] per tile
+  uint64_t* o_done = bars + 13;  // [2] per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int tile = p.tiles[2 * blockIdx.x];
+  const int head = p.tiles[2 * blockIdx.x + 1];
+  const int seq = tile >> 16;
+  const int pair = tile & 0xFFFF;
+  const int seq_start = p.cu_seqlens[seq];
+  const int seqlen = p.cu_seqlens[seq + 1] - seq_start;
+  const int q0 = pair * 256;
+  const bool has_b = q0 + 128 < seqlen;
+  const int n_a = 2 * pair + 1;                 // kv tiles seen by tile A (causal)
+  const int n_b = has_b ? 2 * pair + 2 : 0;     // ... by tile B
+  const int n_kv = has_b ? n_b : n_a;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_q, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 4);
+      mbar_init(o_done + i, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      mbar_expect_tx(bar_q, (has_b ? 2 : 1) * L::kTileBytes);
+      for (int b = 0; b < 2; ++b) {
+        tma_load_3d(smem + L::kQA + b * 16384, &tm_q, bar_q, b * 64, head, seq_start + q0);
+        if (has_b)
+          tma_load_3d(smem + L::kQB + b * 16384, &tm_q, bar_q, b * 64, head, seq_start + q0 + 128);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        const int row = seq_start + j * 128;
+        mbar_wait(k_empty + st, ph ^ 1);
+        mbar_expect_tx(k_full + st, L::kTileBytes);
+        for (int b = 0; b < 2; ++b)
+          tma_load_3d(smem + L::kK + st * L::kTileBytes + b * 16384, &tm_k, k_full + st, b * 64,
+                      head, row);
+        mbar_wait(v_empty + st, ph ^ 1);
+        mbar_expect_tx(v_full + st, L::kTileBytes);
+        for (int b = 0; b < 2; ++b)
+          tma_load_3d(smem + L::kV + st * L::kTileBytes + b * 16384, &tm_v, v_full + st, b * 64,
+                      head, row);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
+      const uint32_t qa = smem_u32(smem + L::kQA), qb = smem_u32(smem + L::kQB);
+      const uint32_t k_base = smem_u32(smem + L::kK);
+      const uint32_t v_base = smem_u32(smem + L::kV);
+      mbar_wait(bar_q, 0);
+      auto qk = [&](int x, int j) {  // S_x = Q_x K_j^T
+        const uint32_t qbase = x ? qb : qa;
+        const uint32_t kb = k_base + (j & 1) * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tmem + x * 128, make_sdesc_sw128(qbase + off, 16, 1024),
+                 make_sdesc_sw128(kb + off, 16, 1024), idesc_s, kk > 0);
+        }
+        tc_commit(s_full + x);
+      };
+      auto pv = [&](int x, int j) {  // O_x += P_x V_j
+        const uint32_t vb = v_base + (j & 1) * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8,
+                 make_sdesc_sw128(vb + kk * 2048, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+      };
+      mbar_wait(k_full + 0, 0);
+      tc_fence_after();
+      qk(0, 0);
+      if (n_b > 0) qk(1, 0);
+      tc_commit(k_empty + 0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        const bool next = j + 1 < n_kv;
+        mbar_wait(v_full + st, (j >> 1) & 1);
+        if (next) mbar_wait(k_full + (st ^ 1), ((j + 1) >> 1) & 1);
+        if (j < n_a) {
+          mbar_wait(p_full + 0, j & 1);
+          tc_fence_after();
+          pv(0, j);
+          if (j + 1 < n_a) qk(0, j + 1);
+          else tc_commit(o_done + 0);
+        }
+        if (j < n_b) {
+          mbar_wait(p_full + 1, j & 1);
+          tc_fence_after();
+          pv(1, j);
+          if (j + 1 < n_b) qk(1, j + 1);
+          else tc_commit(o_done + 1);
+        }
+        tc_commit(v_empty + st);
+        if (next) tc_commit(k_empty + (st ^ 1));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int x = (warp - 2) >> 2;        // 0 -> tile A, 1 -> tile B
+    const uint32_t quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_addr = (quad * 32u) << 16;
+    const uint32_t s_col = x * 128, o_col = 256 + x * 128;
+    const int q_pos = q0 + x * 128 + row;
+    const int n_x = x ? n_b : n_a;
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY;  // exponent base (scaled, log2 units)
+    float l = 0.f;
+    for (int j = 0; j < n_x; ++j) {
+      mbar_wait(s_full + x, j & 1);
+      tc_fence_after();
+      // pass 1: row max over the 128 scores (chunked TMEM loads keep registers free)
+      const bool diag = (j == n_x - 1);
+      const int lim = q_pos - j * 128;  // causal: column c valid iff c <= lim (diagonal tile)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_addr + s_col + c, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (!diag || c + i <= lim) mx = fmaxf(mx, __uint_as_float(r[i]));
+      }
+      const float m_new = fmaxf(m, mx * sl2);
+      // warp-uniform lazy rescale decision (TMEM access is warp-collective)
+      const bool grow = __any_sync(0xffffffffu, m_new > m + 8.f);
+      float corr = 1.f;
+      if (grow) {
+        corr = ex2(m - m_new);  // 0 on the first tile (m = -inf)
+        if (j > 0) {
+#pragma unroll
+          for (int c = 0; c < D; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + lane_addr + o_col + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+            tmem_st32(tmem + lane_addr + o_col + c, r);
+          }
+        }
+        m = m_new;
+      }
+      float sum = 0.f;
+      // pass 2: reload each 32-column chunk, exponentiate, write P (bf16 pairs) back over
+      // S columns [c/2, c/2+16) — all of which this thread has already consumed.
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t r[32], pk[16];
+        tmem_ld32(tmem + lane_addr + s_col + c, r);
+        tmem_ld_wait();
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = c + i <= lim ? ex2(fmaf(__uint_as_float(r[i]), sl2, -m)) : 0.f;
+            const float p1 = c + i + 1 <= lim ? ex2(fmaf(__uint_as_float(r[i + 1]), sl2, -m)) : 0.f;
+            sum += p0 + p1;
+            pk[i / 2] = pack_bf16(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(r[i]), sl2, -m));
+            const float x1 = fmaf(__uint_as_float(r[i + 1]), sl2, -m);
+            const float p1 = (i & 2) ? ex2_poly(x1) : ex2(x1);
+            sum += p0 + p1;
+            pk[i / 2] = pack_bf16(p0, p1);
+          }
+        }
+        tmem_st16(tmem + lane_addr + s_col + c / 2, pk);
+      }
+      l = l * corr + sum;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full + x);
+    }
+    // ------------------------------------------------------------ epilogue
+    if (n_x > 0) {
+      mbar_wait(o_done + x, 0);
+      tc_fence_after();
+      const float inv_l = 1.f / l;
+      const bool valid = q_pos < seqlen;
+      __nv_bfloat16* orow = p.o + (int64_t)(seq_start + q_pos) * p.o_stride + (int64_t)head * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_addr + o_col + c, r);
+        tmem_ld_wait();
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
+            v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+            v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
+            v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + c + i) = v;
+          }
+        }
+      }
+      if (valid)
+        p.lse[(int64_t)head * p.total_rows + seq_start + q_pos] =
+            (m + __log2f(l)) * 0.69314718055994531f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free<512>(tmem);
+}
+
 }  // namespace
 
 // Tensor map over one bf16 operand of a token-major packed buffer:
@@ -304,9 +595,15 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   p.total_rows = a->total_rows;
   p.n_heads = a->n_heads;
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
-  const int smem = FwdSmem<D>::kBytes + 1024;
-  FSP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  attn_fwd_kernel<D><<<(unsigned)a->n_tiles, kFwdThreads, smem, stream>>>(tq, tk, tv, p);
+  if (D == 128) {  // schedule entries are 256-row tile pairs (fsp_attn_schedule, head_dim 128)
+    const int smem = Fwd2Smem::kBytes + 1024;
+    FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attn_fwd_pair_kernel<<<(unsigned)a->n_tiles, kF2Threads, smem, stream>>>(tq, tk, tv, p);
+  } else {
+    const int smem = FwdSmem<D>::kBytes + 1024;
+    FSP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attn_fwd_kernel<D><<<(unsigned)a->n_tiles, kFwdThreads, smem, stream>>>(tq, tk, tv, p);
+  }
   FSP_LAUNCH_CHECK();
   return FSP_OK;
 }
@@ -328,17 +625,22 @@ int check_attn_common(const void* q, const void* k, const void* v, int64_t qs, i
 }  // namespace fsp
 
 extern "C" int32_t fsp_attn_schedule(const int32_t* cu, int32_t n_seq, int32_t n_heads,
-                                     int32_t reverse_causal, int32_t* tiles, int32_t capacity) {
+                                     int32_t head_dim, int32_t kind, int32_t* tiles,
+                                     int32_t capacity) {
   using namespace fsp;
   FSP_CHECK_ARG(cu != nullptr || n_seq == 0, "null cu_seqlens");
   FSP_CHECK_ARG(n_seq >= 0 && n_seq < 65536, "n_seq must be in [0, 65536)");
   FSP_CHECK_ARG(n_heads >= 1, "n_heads must be >= 1");
+  FSP_CHECK_ARG(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
+  FSP_CHECK_ARG(kind == FSP_SCHED_FWD || kind == FSP_SCHED_BWD, "unknown schedule kind %d", kind);
   if (n_seq > 0) FSP_CHECK_ARG(cu[0] == 0, "cu_seqlens[0] must be 0");
+  // forward with head_dim 128 runs 256-row tile pairs (attn_fwd_pair_kernel)
+  const int unit = (kind == FSP_SCHED_FWD && head_dim == 128) ? 2 * kBM : kBM;
   int64_t n = 0;
   for (int s = 0; s < n_seq; ++s) {
     const int len = cu[s + 1] - cu[s];
     FSP_CHECK_ARG(len >= 0, "cu_seqlens must be non-decreasing (sequence %d)", s);
-    const int nt = (len + kBM - 1) / kBM;
+    const int nt = (len + unit - 1) / unit;
     FSP_CHECK_ARG(nt < 65536, "sequence %d too long (%d tokens)", s, len);
     n += nt;
   }
@@ -360,10 +662,10 @@ extern "C" int32_t fsp_attn_schedule(const int32_t* cu, int32_t n_seq, int32_t n
   int64_t k = 0;
   for (int i = 0; i < n_seq; ++i) {
     const int s = order[i];
-    const int nt = (cu[s + 1] - cu[s] + kBM - 1) / kBM;
+    const int nt = (cu[s + 1] - cu[s] + unit - 1) / unit;
     for (int h = 0; h < n_heads; ++h)
       for (int j = 0; j < nt; ++j) {
-        const int t = reverse_causal ? j : nt - 1 - j;
+        const int t = kind == FSP_SCHED_BWD ? j : nt - 1 - j;
         tiles[2 * k] = (s << 16) | t;
         tiles[2 * k + 1] = h;
         ++k;

@@ -137,7 +137,8 @@ class FlexSPExecutor:
                     np.ascontiguousarray(grp.unpack_table().reshape(-1))).to(self.device)
                 rmb.sched = ops.AttnSchedule.build(grp.cu_seqlens, self.device,
                                                    self.n_heads // grp.degree,
-                                                   total_rows=grp.padded_tokens)
+                                                   total_rows=grp.padded_tokens,
+                                                   head_dim=self.head_dim)
                 seg = np.diff(grp.cu_seqlens).astype(np.float64)
                 rmb.fwd_flops = 2.0 * self.head_dim * (self.n_heads // grp.degree) * float((seg ** 2).sum())
                 mbs.append(rmb)

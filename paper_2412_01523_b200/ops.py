@@ -66,6 +66,7 @@ class AttnSchedule:
     bwd_tiles: torch.Tensor       # int32 [2 * n_bwd] device
     n_seq: int
     n_heads: int
+    head_dim: int
     total_rows: int
     max_seqlen: int
 
@@ -78,7 +79,8 @@ class AttnSchedule:
         return self.bwd_tiles.numel() // 2
 
     @staticmethod
-    def build(cu_seqlens_host, device, n_heads: int, total_rows: int | None = None) -> "AttnSchedule":
+    def build(cu_seqlens_host, device, n_heads: int, total_rows: int | None = None,
+              head_dim: int = 128) -> "AttnSchedule":
         """`total_rows` >= cu[-1] lets the packed buffer carry trailing pad rows."""
         cu = np.ascontiguousarray(np.asarray(cu_seqlens_host, dtype=np.int32))
         n_seq = len(cu) - 1
@@ -88,18 +90,19 @@ class AttnSchedule:
         lib = capi.load()
         cu_p = cu.ctypes.data_as(_i32p)
         tiles = []
-        for rev in (0, 1):
-            n = lib.fsp_attn_schedule(cu_p, n_seq, n_heads, rev, None, 0)
+        for kind in (capi.FSP_SCHED_FWD, capi.FSP_SCHED_BWD):
+            n = lib.fsp_attn_schedule(cu_p, n_seq, n_heads, head_dim, kind, None, 0)
             if n < 0:
                 capi.check(n)
             buf = np.zeros(max(2 * n, 2), dtype=np.int32)
-            got = lib.fsp_attn_schedule(cu_p, n_seq, n_heads, rev, buf.ctypes.data_as(_i32p), n)
+            got = lib.fsp_attn_schedule(cu_p, n_seq, n_heads, head_dim, kind,
+                                        buf.ctypes.data_as(_i32p), n)
             if got < 0:
                 capi.check(got)
             tiles.append(torch.from_numpy(buf[:2 * n].copy()).to(device))
         lens = np.diff(cu)
         return AttnSchedule(torch.from_numpy(cu.copy()).to(device), tiles[0], tiles[1], n_seq,
-                            n_heads, rows, int(lens.max()) if n_seq else 0)
+                            n_heads, head_dim, rows, int(lens.max()) if n_seq else 0)
 
 
 def _rows_view_ok(t: torch.Tensor, H: int, D: int) -> None:
@@ -116,9 +119,9 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
     T, H, D = q.shape
     for t in (q, k, v):
         _rows_view_ok(t, H, D)
-    if T != sched.total_rows or H != sched.n_heads:
-        raise ValueError(f"q is [{T}, {H}, .] but the schedule covers {sched.total_rows} rows, "
-                         f"{sched.n_heads} heads")
+    if T != sched.total_rows or H != sched.n_heads or D != sched.head_dim:
+        raise ValueError(f"q is [{T}, {H}, {D}] but the schedule was built for "
+                         f"[{sched.total_rows}, {sched.n_heads}, {sched.head_dim}]")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(D)
     o = out if out is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=q.device)
     lse = torch.empty((H, T), dtype=torch.float32, device=q.device)
@@ -141,9 +144,9 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
     T, H, D = q.shape
     for t in (q, k, v, o, dout):
         _rows_view_ok(t, H, D)
-    if T != sched.total_rows or H != sched.n_heads:
-        raise ValueError(f"q is [{T}, {H}, .] but the schedule covers {sched.total_rows} rows, "
-                         f"{sched.n_heads} heads")
+    if T != sched.total_rows or H != sched.n_heads or D != sched.head_dim:
+        raise ValueError(f"q is [{T}, {H}, {D}] but the schedule was built for "
+                         f"[{sched.total_rows}, {sched.n_heads}, {sched.head_dim}]")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(D)
     dev = q.device
     dq = dq if dq is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)

@@ -26,7 +26,7 @@ print("T", T, "sum s^2", ss)
 dev = torch.device("cuda")
 qkv = torch.randn(T, 3, H, D, device=dev, dtype=torch.bfloat16)
 do = torch.randn(T, H, D, device=dev, dtype=torch.bfloat16)
-sched = ops.AttnSchedule.build(cu, dev, H)
+sched = ops.AttnSchedule.build(cu, dev, H, head_dim=D)
 q, k, v = qkv[:, 0], qkv[:, 1], qkv[:, 2]
 fl_fwd = 2 * D * H * ss  # causal half counted: 4*D*H*s^2/2
 ms = timeit(lambda: ops.attn_fwd(q, k, v, sched))

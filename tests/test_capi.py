@@ -31,13 +31,13 @@ def test_exports_every_declared_symbol(lib):
     assert lib.fsp_abi_version() == 1
 
 
-def _schedule(lib, lens, rev, heads=1):
+def _schedule(lib, lens, rev, heads=1, head_dim=64):
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     p = cu.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    n = lib.fsp_attn_schedule(p, len(lens), heads, rev, None, 0)
+    n = lib.fsp_attn_schedule(p, len(lens), heads, head_dim, rev, None, 0)
     buf = np.zeros(max(2 * n, 2), dtype=np.int32)
     ptr = buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    assert lib.fsp_attn_schedule(p, len(lens), heads, rev, ptr, n) == n
+    assert lib.fsp_attn_schedule(p, len(lens), heads, head_dim, rev, ptr, n) == n
     return [(int(buf[2 * i]) >> 16, int(buf[2 * i]) & 0xFFFF, int(buf[2 * i + 1])) for i in range(n)]
 
 
@@ -61,6 +61,14 @@ def test_schedule_complete_and_ordered(lib, rev):
             assert costs == sorted(costs, reverse=True)
 
 
+def test_forward_schedule_pairs_for_head_dim_128(lib):
+    lens = [1, 128, 129, 300, 1000]
+    tiles = _schedule(lib, lens, 0, heads=2, head_dim=128)
+    npairs = [-(-s // 256) for s in lens]
+    assert sorted(tiles) == sorted((s, t, h) for s, n in enumerate(npairs) for t in range(n)
+                                   for h in range(2))
+
+
 def test_invalid_arguments_raise_valueerror(lib):
     from paper_2412_01523_b200 import capi
     # row_bytes not a multiple of 16 -> rejected on the host before any CUDA call
@@ -78,7 +86,7 @@ def test_invalid_arguments_raise_valueerror(lib):
     ptrs = (ctypes.c_void_p * 3)(16, 16, 16)
     assert lib.fsp_a2a_seq2head(ctypes.byref(x), 16, ptrs, None, None) == capi.FSP_ERR_INVALID
     cu = (ctypes.c_int32 * 3)(0, 5, 3)  # decreasing cu_seqlens
-    assert lib.fsp_attn_schedule(cu, 2, 1, 0, None, 0) == capi.FSP_ERR_INVALID
+    assert lib.fsp_attn_schedule(cu, 2, 1, 64, 0, None, 0) == capi.FSP_ERR_INVALID
 
 
 def test_device_ops_reject_cpu_tensors(lib):

@@ -70,7 +70,7 @@ def test_attn_fwd_matches_oracle(lengths, H, D):
     cu, qkv = _rand_qkv(lengths, H, D, seed=sum(lengths) + H)
     dev = torch.device("cuda")
     qkv_d = qkv.to(dev)
-    sched = ops.AttnSchedule.build(cu, dev, H)
+    sched = ops.AttnSchedule.build(cu, dev, H, head_dim=D)
     o, lse = ops.attn_fwd(qkv_d[:, 0], qkv_d[:, 1], qkv_d[:, 2], sched)
     torch.cuda.synchronize()
     o_ref, lse_ref = attention_fwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], cu)
@@ -95,7 +95,7 @@ def test_attn_bwd_matches_oracle(lengths, H, D):
     dout = torch.randn(int(cu[-1]), H, D, generator=g).bfloat16()
     dev = torch.device("cuda")
     qkv_d = qkv.to(dev)
-    sched = ops.AttnSchedule.build(cu, dev, H)
+    sched = ops.AttnSchedule.build(cu, dev, H, head_dim=D)
     q, k, v = qkv_d[:, 0], qkv_d[:, 1], qkv_d[:, 2]
     o, lse = ops.attn_fwd(q, k, v, sched)
     dq, dk, dv = ops.attn_bwd(q, k, v, o, dout.to(dev), lse, sched)

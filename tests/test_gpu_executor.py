@@ -137,7 +137,7 @@ def test_attention_golden_vectors():
     z = np.load(GOLDEN / "attn_small.npz")
     bf = lambda a: torch.from_numpy(a).view(torch.bfloat16).cuda()  # noqa: E731
     q, k, v, do = bf(z["q"]), bf(z["k"]), bf(z["v"]), bf(z["do"])
-    sched = ops.AttnSchedule.build(z["cu_seqlens"], "cuda", 1)
+    sched = ops.AttnSchedule.build(z["cu_seqlens"], "cuda", 1, head_dim=64)
     o, lse = ops.attn_fwd(q, k, v, sched)
     dq, dk, dv = ops.attn_bwd(q, k, v, o, do, lse, sched)
     torch.cuda.synchronize()
