@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       const int q0 = (kt + it) * kTile;
       const bool valid = q0 + t < seqlen;
       const int64_t gi = (int64_t)head * p.total_rows + seq_start + q0 + t;
-      if (ctid < 128) return valid ? p.lse[gi] * kLog2e : INFINITY;
+      if (ctid < 128) return valid ? -p.lse[gi] * kLog2e : -INFINITY;  // stored negated
       return valid ? p.delta[gi] : 0.f;
     };
     auto half = [&](auto diag_c, int it, int h) {
@@ -601,17 +601,26 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       // both column halves of every lane must be read before P^T overwrites S
       named_bar_sync(2 + h, 32 * kV2Compute);
       uint32_t pk[16], dk[16];
+      const uint64_t sl2x2 = f2(sl2, sl2);
+      const uint64_t* nls2 = reinterpret_cast<const uint64_t*>(ls);  // -lse*log2e pairs
+      const uint64_t* dl2 = reinterpret_cast<const uint64_t*>(dl);
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
-        float p0 = ex2(fmaf(__uint_as_float(sr[i]), sl2, -ls[i]));
-        float p1 = ex2(fmaf(__uint_as_float(sr[i + 1]), sl2, -ls[i + 1]));
+        const uint64_t x2 =
+            ffma2(f2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sl2x2, nls2[i / 2]);
+        float x0, x1;
+        f2_split(x2, x0, x1);
+        float p0 = ex2(x0), p1 = ex2(x1);
         if (kDiag) {  // causal on the diagonal tile: query column c0+i >= kv row r
           if (c0 + i < r) p0 = 0.f;
           if (c0 + i + 1 < r) p1 = 0.f;
         }
+        const uint64_t ds2 = fmul2(
+            f2(p0, p1), fsub2(f2(__uint_as_float(dr[i]), __uint_as_float(dr[i + 1])), dl2[i / 2]));
+        float d0, d1;
+        f2_split(ds2, d0, d1);
         pk[i / 2] = pack_bf16(p0, p1);
-        dk[i / 2] = pack_bf16(p0 * (__uint_as_float(dr[i]) - dl[i]),
-                              p1 * (__uint_as_float(dr[i + 1]) - dl[i + 1]));
+        dk[i / 2] = pack_bf16(d0, d1);
       }
       tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, pk);
       // dS^T row r, query columns [ch*32, ch*32+32) of this half: 16-byte chunks 4ch+v

@@ -13,6 +13,7 @@
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O [256,256+D) P0 [384,448) P1 [448,512).
 // S is double-buffered so QK^T of tile j+1 overlaps the softmax of tile j.
 #include <algorithm>
+#include <type_traits>
 
 #include "fsp_host.h"
 #include "fsp_ptx.cuh"
@@ -291,14 +292,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // 16/clk/SM MUFU.EX2 rate would otherwise equal the tensor-core time per tile).
 // TMEM: S_A|P_A [0,128) S_B|P_B [128,256) O_A [256,384) O_B [384,512).
 constexpr int kF2Threads = 64 + 256;
+#ifndef FSP_ABLATE_EXP
+#define FSP_ABLATE_EXP 0
+#endif
 
 struct Fwd2Smem {
   static constexpr int kTileBytes = 128 * 128 * 2;
   static constexpr int kQA = 0;
   static constexpr int kQB = kTileBytes;
-  static constexpr int kK = 2 * kTileBytes;  // 2 stages
-  static constexpr int kV = 4 * kTileBytes;  // 2 stages
-  static constexpr int kBar = 6 * kTileBytes;
+  static constexpr int kKStages = 3;  // K runs a stage ahead of V (S needs K_{j+1} first)
+  static constexpr int kK = 2 * kTileBytes;
+  static constexpr int kV = kK + kKStages * kTileBytes;  // 2 stages
+  static constexpr int kBar = kV + 2 * kTileBytes;
   static constexpr int kBytes = kBar + 256;
 };
 
@@ -325,14 +330,14 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* bar_q = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2]
-  uint64_t* v_full = bars + 5;   // [2]
-  uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2] per tile
-  uint64_t* p_full = bars + 11;  // [2] per tile
-  uint64_t* o_done = bars + 13;  // [2] per tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* k_full = bars + 1;   // [3]
+  uint64_t* k_empty = bars + 4;  // [3]
+  uint64_t* v_full = bars + 7;   // [2]
+  uint64_t* v_empty = bars + 9;  // [2]
+  uint64_t* s_full = bars + 11;  // [2] per tile
+  uint64_t* p_full = bars + 13;  // [2] per tile
+  uint64_t* o_done = bars + 15;  // [2] per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -350,9 +355,11 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < L::kKStages; ++i) {
       mbar_init(k_full + i, 1);
       mbar_init(k_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(v_full + i, 1);
       mbar_init(v_empty + i, 1);
       mbar_init(s_full + i, 1);
@@ -379,20 +386,24 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         if (has_b)
           tma_load_3d(smem + L::kQB + b * 16384, &tm_q, bar_q, b * 64, head, seq_start + q0 + 128);
       }
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        const int row = seq_start + j * 128;
-        mbar_wait(k_empty + st, ph ^ 1);
+      // issue order K_0, K_1, V_0, K_2, V_1, ...: K is consumed one step before V
+      auto load_k = [&](int j) {
+        const int st = j % L::kKStages;
+        mbar_wait(k_empty + st, ((j / L::kKStages) & 1) ^ 1);
         mbar_expect_tx(k_full + st, L::kTileBytes);
         for (int b = 0; b < 2; ++b)
           tma_load_3d(smem + L::kK + st * L::kTileBytes + b * 16384, &tm_k, k_full + st, b * 64,
-                      head, row);
-        mbar_wait(v_empty + st, ph ^ 1);
+                      head, seq_start + j * 128);
+      };
+      load_k(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) load_k(j + 1);
+        const int st = j & 1;
+        mbar_wait(v_empty + st, ((j >> 1) & 1) ^ 1);
         mbar_expect_tx(v_full + st, L::kTileBytes);
         for (int b = 0; b < 2; ++b)
           tma_load_3d(smem + L::kV + st * L::kTileBytes + b * 16384, &tm_v, v_full + st, b * 64,
-                      head, row);
+                      head, seq_start + j * 128);
       }
     }
     __syncwarp();
@@ -407,7 +418,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       mbar_wait(bar_q, 0);
       auto qk = [&](int x, int j) {  // S_x = Q_x K_j^T
         const uint32_t qbase = x ? qb : qa;
-        const uint32_t kb = k_base + (j & 1) * L::kTileBytes;
+        const uint32_t kb = k_base + (j % L::kKStages) * L::kTileBytes;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -423,8 +434,11 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           mma_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8,
                  make_sdesc_sw128(vb + kk * 2048, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
       };
-      mbar_wait(k_full + 0, 0);
-      tc_fence_after();
+      auto wait_k = [&](int j) {
+        mbar_wait(k_full + j % L::kKStages, (j / L::kKStages) & 1);
+        tc_fence_after();
+      };
+      wait_k(0);
       qk(0, 0);
       if (n_b > 0) qk(1, 0);
       tc_commit(k_empty + 0);
@@ -432,23 +446,30 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         const int st = j & 1;
         const bool next = j + 1 < n_kv;
         mbar_wait(v_full + st, (j >> 1) & 1);
-        if (next) mbar_wait(k_full + (st ^ 1), ((j + 1) >> 1) & 1);
         if (j < n_a) {
           mbar_wait(p_full + 0, j & 1);
           tc_fence_after();
           pv(0, j);
-          if (j + 1 < n_a) qk(0, j + 1);
-          else tc_commit(o_done + 0);
+          if (j + 1 < n_a) {
+            wait_k(j + 1);
+            qk(0, j + 1);
+          } else {
+            tc_commit(o_done + 0);
+          }
         }
         if (j < n_b) {
           mbar_wait(p_full + 1, j & 1);
           tc_fence_after();
           pv(1, j);
-          if (j + 1 < n_b) qk(1, j + 1);
-          else tc_commit(o_done + 1);
+          if (j + 1 < n_b) {
+            wait_k(j + 1);
+            qk(1, j + 1);
+          } else {
+            tc_commit(o_done + 1);
+          }
         }
         tc_commit(v_empty + st);
-        if (next) tc_commit(k_empty + (st ^ 1));
+        if (next) tc_commit(k_empty + (j + 1) % L::kKStages);
       }
     }
     __syncwarp();
@@ -467,67 +488,121 @@ __global__ void __launch_bounds__(kF2Threads, 1)
     for (int j = 0; j < n_x; ++j) {
       mbar_wait(s_full + x, j & 1);
       tc_fence_after();
-      // pass 1: row max over the 128 scores (chunked TMEM loads keep registers free)
-      const bool diag = (j == n_x - 1);
+      if (FSP_ABLATE_EXP >= 2) {  // profiling ablations: 2 = no softmax work,
+        // 3 = two passes of TMEM loads + P store, 4 = one pass of loads + P store
+        if (FSP_ABLATE_EXP >= 3) {
+          uint32_t acc = 0;
+#pragma unroll
+          for (int pass = 0; pass < (FSP_ABLATE_EXP == 3 ? 2 : 1); ++pass)
+#pragma unroll
+            for (int c = 0; c < 128; c += 32) {
+              uint32_t r[32];
+              tmem_ld32(tmem + lane_addr + s_col + c, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) acc ^= r[i];
+            }
+#pragma unroll
+          for (int c = 0; c < 64; c += 16) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = acc + i;
+            tmem_st16(tmem + lane_addr + s_col + c, pk);
+          }
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full + x);
+        continue;
+      }
+      // The diagonal tile (causal mask) and the interior tiles get separate straight-line
+      // code: per-pair masking branches would serialise the MUFU / FFMA2 streams.
       const int lim = q_pos - j * 128;  // causal: column c valid iff c <= lim (diagonal tile)
-      float mx = -INFINITY;
+      auto tile_body = [&](auto diag_c) {
+        constexpr bool kDiag = decltype(diag_c)::value;
+        // pass 1: row max; four independent FMNMX3 chains, chunked TMEM loads
+        float mxs[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_addr + s_col + c, r);
-        tmem_ld_wait();
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_addr + s_col + c, r);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (!diag || c + i <= lim) mx = fmaxf(mx, __uint_as_float(r[i]));
-      }
-      const float m_new = fmaxf(m, mx * sl2);
-      // warp-uniform lazy rescale decision (TMEM access is warp-collective)
-      const bool grow = __any_sync(0xffffffffu, m_new > m + 8.f);
-      float corr = 1.f;
-      if (grow) {
-        corr = ex2(m - m_new);  // 0 on the first tile (m = -inf)
-        if (j > 0) {
+          for (int i = 0; i < 32; i += 8)
 #pragma unroll
-          for (int c = 0; c < D; c += 32) {
-            uint32_t r[32];
-            tmem_ld32(tmem + lane_addr + o_col + c, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
-            tmem_st32(tmem + lane_addr + o_col + c, r);
-          }
+            for (int a = 0; a < 4; ++a) {
+              float v0 = __uint_as_float(r[i + 2 * a]), v1 = __uint_as_float(r[i + 2 * a + 1]);
+              if (kDiag) {
+                v0 = c + i + 2 * a <= lim ? v0 : -INFINITY;
+                v1 = c + i + 2 * a + 1 <= lim ? v1 : -INFINITY;
+              }
+              mxs[a] = fmax3(mxs[a], v0, v1);
+            }
         }
-        m = m_new;
-      }
-      float sum = 0.f;
-      // pass 2: reload each 32-column chunk, exponentiate, write P (bf16 pairs) back over
-      // S columns [c/2, c/2+16) — all of which this thread has already consumed.
+        const float mx = fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3]));
+        const float m_new = fmaxf(m, mx * sl2);
+        // warp-uniform lazy rescale decision (TMEM access is warp-collective)
+        const bool grow = __any_sync(0xffffffffu, m_new > m + 8.f);
+        float corr = 1.f;
+        if (grow) {
+          corr = ex2(m - m_new);  // 0 on the first tile (m = -inf)
+          if (j > 0) {
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t r[32], pk[16];
-        tmem_ld32(tmem + lane_addr + s_col + c, r);
-        tmem_ld_wait();
-        if (diag) {
+            for (int c = 0; c < D; c += 32) {
+              uint32_t r[32];
+              tmem_ld32(tmem + lane_addr + o_col + c, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+              tmem_st32(tmem + lane_addr + o_col + c, r);
+            }
+          }
+          m = m_new;
+        }
+        // pass 2: reload each 32-column chunk, exponentiate, write P (bf16 pairs) back over
+        // S columns [c/2, c/2+16) — all of which this thread has already consumed.
+        // Packed fp32x2 math; one pair in four exponentiates on the FMA pipe (ex2_poly2).
+        const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(-m, -m);
+        uint64_t sum2[4] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t r[32], pk[16];
+          tmem_ld32(tmem + lane_addr + s_col + c, r);
+          tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
-            const float p0 = c + i <= lim ? ex2(fmaf(__uint_as_float(r[i]), sl2, -m)) : 0.f;
-            const float p1 = c + i + 1 <= lim ? ex2(fmaf(__uint_as_float(r[i + 1]), sl2, -m)) : 0.f;
-            sum += p0 + p1;
+            const uint64_t x2 =
+                ffma2(f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, negm2);
+            float p0, p1;
+            if (kDiag) {
+              float x0, x1;
+              f2_split(x2, x0, x1);
+              p0 = ex2(c + i <= lim ? x0 : -INFINITY);
+              p1 = ex2(c + i + 1 <= lim ? x1 : -INFINITY);
+            } else if (FSP_ABLATE_EXP) {  // profiling ablation: no exponentials
+              f2_split(x2, p0, p1);
+            } else if ((i & 6) == 6) {
+              ex2_poly2(x2, p0, p1);
+            } else {
+              float x0, x1;
+              f2_split(x2, x0, x1);
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            sum2[(i >> 1) & 3] = fadd2(sum2[(i >> 1) & 3], f2(p0, p1));
             pk[i / 2] = pack_bf16(p0, p1);
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float p0 = ex2(fmaf(__uint_as_float(r[i]), sl2, -m));
-            const float x1 = fmaf(__uint_as_float(r[i + 1]), sl2, -m);
-            const float p1 = (i & 2) ? ex2_poly(x1) : ex2(x1);
-            sum += p0 + p1;
-            pk[i / 2] = pack_bf16(p0, p1);
-          }
+          tmem_st16(tmem + lane_addr + s_col + c / 2, pk);
         }
-        tmem_st16(tmem + lane_addr + s_col + c / 2, pk);
-      }
-      l = l * corr + sum;
+        float sum_lo, sum_hi;
+        f2_split(fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3])), sum_lo, sum_hi);
+        l = l * corr + (sum_lo + sum_hi);
+      };
+      if (j == n_x - 1)
+        tile_body(std::true_type{});
+      else
+        tile_body(std::false_type{});
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();

@@ -19,7 +19,12 @@ def timeit(fn, iters=10, warm=3):
     return s.elapsed_time(e) / iters
 
 H, D = int(os.environ.get("H", 32)), 128
-L = lengths_c2()
+WL = os.environ.get("WL", "c2")
+if WL == "c2":
+    L = lengths_c2()
+else:  # e.g. WL=32768x8 : uniform lengths
+    n, k = WL.split("x")
+    L = np.full(int(k), int(n))
 cu = np.concatenate([[0], np.cumsum(L)]).astype(np.int32)
 T = int(cu[-1]); ss = float((L.astype(np.float64)**2).sum())
 print("T", T, "sum s^2", ss)
@@ -37,6 +42,8 @@ try:
     print(f"fsp bwd: {ms:.3f} ms  {2.5*fl_fwd/ms/1e9:.1f} TFLOP/s")
 except Exception as ex:
     print("bwd:", ex)
+if os.environ.get("NOFA"):
+    raise SystemExit(0)
 try:
     from flash_attn import flash_attn_varlen_func
     cu_t = torch.from_numpy(cu).to(dev)
