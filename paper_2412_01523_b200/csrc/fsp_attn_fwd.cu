@@ -295,6 +295,10 @@ constexpr int kF2Threads = 64 + 256;
 #ifndef FSP_ABLATE_EXP
 #define FSP_ABLATE_EXP 0
 #endif
+// one exponential pair in FSP_POLY_EVERY runs as a polynomial on the FMA pipe (0 = none)
+#ifndef FSP_POLY_EVERY
+#define FSP_POLY_EVERY 4
+#endif
 
 struct Fwd2Smem {
   static constexpr int kTileBytes = 128 * 128 * 2;
@@ -335,9 +339,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   uint64_t* v_full = bars + 7;   // [2]
   uint64_t* v_empty = bars + 9;  // [2]
   uint64_t* s_full = bars + 11;  // [2] per tile
-  uint64_t* p_full = bars + 13;  // [2] per tile
-  uint64_t* o_done = bars + 15;  // [2] per tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* o_done = bars + 13;  // [2] per tile
+  uint64_t* p_half = bars + 15;  // [2 tiles][2 halves]: P columns for kv rows 0-63 / 64-127
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -363,7 +367,8 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       mbar_init(v_full + i, 1);
       mbar_init(v_empty + i, 1);
       mbar_init(s_full + i, 1);
-      mbar_init(p_full + i, 4);
+      mbar_init(p_half + 2 * i, 4);
+      mbar_init(p_half + 2 * i + 1, 4);
       mbar_init(o_done + i, 1);
     }
     fence_mbar_init();
@@ -427,12 +432,18 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         }
         tc_commit(s_full + x);
       };
-      auto pv = [&](int x, int j) {  // O_x += P_x V_j
+      auto pv = [&](int x, int j) {  // O_x += P_x V_j, each half as soon as its P lands
         const uint32_t vb = v_base + (j & 1) * L::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8,
-                 make_sdesc_sw128(vb + kk * 2048, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int hh = 0; hh < 2; ++hh) {
+          mbar_wait(p_half + 2 * x + hh, j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
+            mma_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8,
+                   make_sdesc_sw128(vb + kk * 2048, 16384, 1024), idesc_o,
+                   (j > 0 || kk > 0) ? 1u : 0u);
+        }
       };
       auto wait_k = [&](int j) {
         mbar_wait(k_full + j % L::kKStages, (j / L::kKStages) & 1);
@@ -447,8 +458,6 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         const bool next = j + 1 < n_kv;
         mbar_wait(v_full + st, (j >> 1) & 1);
         if (j < n_a) {
-          mbar_wait(p_full + 0, j & 1);
-          tc_fence_after();
           pv(0, j);
           if (j + 1 < n_a) {
             wait_k(j + 1);
@@ -458,8 +467,6 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           }
         }
         if (j < n_b) {
-          mbar_wait(p_full + 1, j & 1);
-          tc_fence_after();
           pv(1, j);
           if (j + 1 < n_b) {
             wait_k(j + 1);
@@ -513,7 +520,10 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full + x);
+        if (lane == 0) {
+          mbar_arrive(p_half + 2 * x);
+          mbar_arrive(p_half + 2 * x + 1);
+        }
         continue;
       }
       // The diagonal tile (causal mask) and the interior tiles get separate straight-line
@@ -582,7 +592,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
               p1 = ex2(c + i + 1 <= lim ? x1 : -INFINITY);
             } else if (FSP_ABLATE_EXP) {  // profiling ablation: no exponentials
               f2_split(x2, p0, p1);
-            } else if ((i & 6) == 6) {
+            } else if (FSP_POLY_EVERY > 0 && (i / 2) % FSP_POLY_EVERY == FSP_POLY_EVERY - 1) {
               ex2_poly2(x2, p0, p1);
             } else {
               float x0, x1;
@@ -594,6 +604,12 @@ __global__ void __launch_bounds__(kF2Threads, 1)
             pk[i / 2] = pack_bf16(p0, p1);
           }
           tmem_st16(tmem + lane_addr + s_col + c / 2, pk);
+          if (c == 32) {  // P for kv rows 0..63 is in TMEM: release the first PV half
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_half + 2 * x);
+          }
         }
         float sum_lo, sum_hi;
         f2_split(fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3])), sum_lo, sum_hi);
@@ -606,7 +622,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full + x);
+      if (lane == 0) mbar_arrive(p_half + 2 * x + 1);
     }
     // ------------------------------------------------------------ epilogue
     if (n_x > 0) {
