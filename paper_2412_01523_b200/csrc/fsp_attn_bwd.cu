@@ -397,6 +397,9 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
 // TMEM: dK [0,128) dV [128,256) S0 [256,320) S1 [320,384) dP0|dQ0 [384,448) dP1|dQ1 [448,512)
 // Warps: 0 TMA, 1 MMA, 2..9 compute (two per TMEM lane quadrant, 32 of the 64 columns
 // each), 10..13 dQ reduction (one per quadrant, all 64 columns).
+#ifndef FSP_BWD_ABLATE
+#define FSP_BWD_ABLATE 0  // profiling ablations: 1 = skip gradient math, 2 = skip dQ readout
+#endif
 constexpr int kV2Compute = 8;
 constexpr int kV2Reduce = 4;
 constexpr int kV2Threads = 64 + 32 * (kV2Compute + kV2Reduce);
@@ -594,6 +597,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       const float* dl = delta_s + buf * 128 + c0;
       mbar_wait(s_full + h, it & 1);
       tc_fence_after();
+      if (FSP_BWD_ABLATE & 1) {  // profiling ablation: no gradient math
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_ready + h);
+        return;
+      }
       uint32_t sr[32], dr[32];
       tmem_ld32(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, sr);
       tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, dr);
@@ -693,6 +702,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       const int it = u >> 1, h = u & 1;
       mbar_wait(dq_full + h, it & 1);
       tc_fence_after();
+      if (FSP_BWD_ABLATE & 2) {  // profiling ablation: no dQ readout / reductions
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tm_free + h);
+        continue;
+      }
       uint32_t qr[64];
       tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64, *reinterpret_cast<uint32_t(*)[32]>(qr));
       tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + 32,
