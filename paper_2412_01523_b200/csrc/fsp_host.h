@@ -37,5 +37,8 @@ void set_error(const char* fmt, ...);
 // byte stride of dims[i+1].
 int encode_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
                      const uint64_t* strides_bytes, const uint32_t* box);
+// Same, any element type (SWIZZLE_128B: the inner box dimension must be 128 bytes).
+int encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, int rank,
+                const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box);
 
 }  // namespace fsp
