@@ -288,3 +288,64 @@ class FlexSPExecutor:
             dqkv = self.micro_batch_backward(sp, mb, saved, dout_locals[m])
             if sink is not None:
                 sink(m, out, dqkv)
+
+    def step_from_host(self, sp: StepPlan, host_qkv: Sequence[torch.Tensor],
+                       host_dout: Sequence[torch.Tensor], sink=None) -> torch.Tensor:
+        """The same step fed straight from pinned host memory (the data-loader path).
+
+        Micro-batch m+1's q/k/v and dO are copied host->device on a side stream into the
+        other half of a double buffer while micro-batch m computes, so PCIe transfer and
+        the SP step overlap.  Returns a device fp32 scalar, the step's <O, dO> "loss"
+        (a cheap reduction over every output, read back by the caller).
+        """
+        cur = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_h2d_stream"):
+            self._h2d_stream = torch.cuda.Stream(self.device)
+        side = self._h2d_stream
+        n = len(sp.micro_batches)
+        hd = self.n_heads * self.head_dim
+        max_rows = max((mb.n_local for mb in sp.micro_batches), default=0)
+        bufs = []
+        for k in range(2):
+            q = self._workspace(f"h2d_qkv{k}", max(max_rows, 1) * 3 * hd, torch.bfloat16)
+            d = self._workspace(f"h2d_do{k}", max(max_rows, 1) * hd, torch.bfloat16)
+            bufs.append((q, d))
+        loaded = [torch.cuda.Event() for _ in range(2)]
+        # persistent across calls: the next step's first copies must not overwrite a buffer
+        # the previous step is still reading (waiting on a never-recorded event is a no-op)
+        if not hasattr(self, "_h2d_consumed"):
+            self._h2d_consumed = [torch.cuda.Event() for _ in range(2)]
+        consumed = self._h2d_consumed
+        loss = torch.zeros((), dtype=torch.float32, device=self.device)
+
+        def issue_copy(m):
+            k = m & 1
+            rows = sp.micro_batches[m].n_local
+            with torch.cuda.stream(side):
+                side.wait_event(consumed[k])
+                q, d = bufs[k]
+                if rows:
+                    q[:rows * 3 * hd].view(rows, 3 * hd).copy_(host_qkv[m].view(rows, 3 * hd),
+                                                                 non_blocking=True)
+                    d[:rows * hd].view(rows, hd).copy_(host_dout[m].view(rows, hd),
+                                                       non_blocking=True)
+                loaded[k].record(side)
+
+        if n:
+            issue_copy(0)
+        for m, mb in enumerate(sp.micro_batches):
+            if m + 1 < n:
+                issue_copy(m + 1)
+            k = m & 1
+            cur.wait_event(loaded[k])
+            rows = mb.n_local
+            q = bufs[k][0][:rows * 3 * hd].view(rows, 3, self.n_heads, self.head_dim)
+            d = bufs[k][1][:rows * hd].view(rows, self.n_heads, self.head_dim)
+            out, saved = self.micro_batch_forward(sp, mb, q)
+            dqkv = self.micro_batch_backward(sp, mb, saved, d)
+            if out is not None and rows:
+                loss += torch.dot(out.reshape(-1).float(), d.reshape(-1).float())
+            if sink is not None:
+                sink(m, out, dqkv)
+            consumed[k].record(cur)
+        return loss

@@ -145,3 +145,36 @@ def test_attention_golden_vectors():
     assert (lse.cpu() - torch.from_numpy(z["lse"])).abs().max() <= 1e-3 * 10
     for got, key in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
         torch.testing.assert_close(got.float().cpu(), torch.from_numpy(z[key]), atol=5e-2, rtol=5e-2)
+
+
+def test_step_from_host_matches_device_step():
+    """The pinned-host, copy-overlapped entry point computes the same step."""
+    from paper_2412_01523_b200.executor import FlexSPExecutor
+    H, D = 4, 128
+    lengths = [700, 1, 130, 2048, 64, 300]
+    plan = _plan_n1(lengths, [[3, 1, 5], [0, 2, 4]])
+    ex = FlexSPExecutor(1, 0, H, D, "cuda")
+    sp = ex.prepare(plan, lengths)
+    T = sum(lengths)
+    g = torch.Generator().manual_seed(3)
+    qkv = torch.randn(T, 3, H, D, generator=g).bfloat16()
+    dout = torch.randn(T, H, D, generator=g).bfloat16()
+    toks = [torch.from_numpy(mb.local_tokens) for mb in sp.micro_batches]
+    res = {}
+
+    def sink_for(tag):
+        def sink(m, out, dqkv):
+            res[(tag, m)] = (out.float().cpu(), dqkv.float().cpu())
+        return sink
+
+    ex.step(sp, [qkv[t].cuda() for t in toks], [dout[t].cuda() for t in toks], sink=sink_for("dev"))
+    hq = [qkv[t].contiguous().pin_memory() for t in toks]
+    hd = [dout[t].contiguous().pin_memory() for t in toks]
+    for _ in range(2):  # twice: buffers are reused across calls
+        loss = ex.step_from_host(sp, hq, hd, sink=sink_for("host"))
+    torch.cuda.synchronize()
+    ref_loss = sum(float((res[("dev", m)][0] * dout[t].float()).sum()) for m, t in enumerate(toks))
+    assert abs(loss.item() - ref_loss) <= 1e-3 * max(1.0, abs(ref_loss))
+    for m in range(len(toks)):
+        torch.testing.assert_close(res[("host", m)][0], res[("dev", m)][0])
+        torch.testing.assert_close(res[("host", m)][1], res[("dev", m)][1], atol=2e-2, rtol=2e-2)
