@@ -520,7 +520,10 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO_h      (K = 64 query rows)
-          mma_ts(tmem + kColDV, tmem + kV2ColS + h * 64 + kk * 8,
+          // P^T of query columns [16kk, 16kk+16): the ch=0 warp wrote columns 0..31 of the
+          // half into S columns [0,16), the ch=1 warp columns 32..63 into [48,64) — each
+          // over S columns it read itself, so no cross-warp barrier is needed
+          mma_ts(tmem + kColDV, tmem + kV2ColS + h * 64 + (kk < 2 ? kk * 8 : 32 + kk * 8),
                  make_sdesc_sw128(do_base + kk * 2048, 8192, 1024), idesc_dvdk,
                  (u > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
@@ -607,8 +610,6 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       tmem_ld32(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, sr);
       tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, dr);
       tmem_ld_wait();
-      // both column halves of every lane must be read before P^T overwrites S
-      named_bar_sync(2 + h, 32 * kV2Compute);
       uint32_t pk[16], dk[16];
       const uint64_t sl2x2 = f2(sl2, sl2);
       const uint64_t* nls2 = reinterpret_cast<const uint64_t*>(ls);  // -lse*log2e pairs
@@ -631,7 +632,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         pk[i / 2] = pack_bf16(p0, p1);
         dk[i / 2] = pack_bf16(d0, d1);
       }
-      tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, pk);
+      tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 48, pk);  // own S columns
       // dS^T row r, query columns [ch*32, ch*32+32) of this half: 16-byte chunks 4ch+v
       uint8_t* row = smem + L::kDS + h * 16384 + r * 128;
 #pragma unroll
