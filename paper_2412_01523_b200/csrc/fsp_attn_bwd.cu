@@ -436,7 +436,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   uint64_t* p_ready = bars + 15;    // [2]
   uint64_t* dq_full = bars + 17;    // [2]
   uint64_t* tm_free = bars + 19;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  uint64_t* acc_done = bars + 21;   // dK / dV final
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       mbar_init(dq_full + i, 1);
       mbar_init(tm_free + i, kV2Reduce);
     }
+    mbar_init(acc_done, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -518,6 +520,15 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         const uint32_t dsb = ds_base + h * 16384;
         mbar_wait(p_ready + h, it & 1);
         tc_fence_after();
+        // dQ^T first and committed on its own, so the reduction warps drain it while dV and
+        // dK (and the next S^T) keep the tensor core busy: dP^T(u+2) waits on that drain.
+        if (u >= 2) mbar_wait(tm_free + h, ((u >> 1) - 1) & 1);  // dQ^T(u-2) drained
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 kv rows)
+          mma_ss(tmem + kV2ColDP + h * 64, make_sdesc_sw128(k_base + kk * 2048, 16384, 1024),
+                 make_sdesc_sw128(dsb + kk * 2048, 16384, 1024), idesc_dqt, kk > 0);
+        tc_commit(dq_full + h);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO_h      (K = 64 query rows)
           // P^T of query columns [16kk, 16kk+16): the ch=0 warp wrote columns 0..31 of the
@@ -531,15 +542,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
           mma_ss(tmem + kColDK, make_sdesc_sw128(dsb + kk * 32, 16, 1024),
                  make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
                  (u > 0 || kk > 0) ? 1u : 0u);
-        if (u >= 2) mbar_wait(tm_free + h, ((u >> 1) - 1) & 1);  // dQ^T(u-2) drained
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 kv rows)
-          mma_ss(tmem + kV2ColDP + h * 64, make_sdesc_sw128(k_base + kk * 2048, 16384, 1024),
-                 make_sdesc_sw128(dsb + kk * 2048, 16384, 1024), idesc_dqt, kk > 0);
-        tc_commit(dq_full + h);
         tc_commit(ring_empty + sq);
         tc_commit(ring_empty + sd);
+        if (u == n_u - 1) tc_commit(acc_done);
       };
       for (int u = 0; u < n_u; ++u) {
         const int h = u & 1;
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       }
     }
     // ---- epilogue: this thread writes D/2 columns of dK (scaled) and dV for kv row r
-    if (n_u > 0) mbar_wait(dq_full + ((n_u - 1) & 1), ((n_u - 1) >> 1) & 1);  // all MMAs done
+    if (n_u > 0) mbar_wait(acc_done, 0);  // all MMAs done
     tc_fence_after();
     {
       const bool kvalid = kv_pos < seqlen;
