@@ -400,7 +400,11 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
 #ifndef FSP_BWD_ABLATE
 #define FSP_BWD_ABLATE 0  // profiling ablations: 1 = skip gradient math, 2 = skip dQ readout
 #endif
-constexpr int kV2Compute = 8;
+#ifndef FSP_BWD_COMPUTE_WARPS
+#define FSP_BWD_COMPUTE_WARPS 16
+#endif
+constexpr int kV2Compute = FSP_BWD_COMPUTE_WARPS;  // 8 or 16: 2 or 4 warps per lane quadrant
+constexpr int kV2Cols = 64 / (kV2Compute / 4);      // query columns per compute warp
 constexpr int kV2Reduce = 4;
 constexpr int kV2Threads = 64 + 32 * (kV2Compute + kV2Reduce);
 constexpr uint32_t kV2ColS = 256, kV2ColDP = 384;
@@ -531,10 +535,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         tc_commit(dq_full + h);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO_h      (K = 64 query rows)
-          // P^T of query columns [16kk, 16kk+16): the ch=0 warp wrote columns 0..31 of the
-          // half into S columns [0,16), the ch=1 warp columns 32..63 into [48,64) — each
-          // over S columns it read itself, so no cross-warp barrier is needed
-          mma_ts(tmem + kColDV, tmem + kV2ColS + h * 64 + (kk < 2 ? kk * 8 : 32 + kk * 8),
+          // P^T of query columns [16kk, 16kk+16): compute warp ch wrote its kV2Cols columns
+          // as bf16 pairs into the first half of its own S columns [ch*kV2Cols, ...) — S
+          // columns it read itself, so no cross-warp barrier is needed
+          mma_ts(tmem + kColDV,
+                 tmem + kV2ColS + h * 64 + (16 * kk / kV2Cols) * kV2Cols + (16 * kk % kV2Cols) / 2,
                  make_sdesc_sw128(do_base + kk * 2048, 8192, 1024), idesc_dvdk,
                  (u > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
@@ -580,14 +585,14 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     __syncwarp();
   } else if (warp < 2 + kV2Compute) {
     // ------------------------------------------------------------ compute warps
-    const uint32_t cw = warp - 2;              // 0..7
+    const uint32_t cw = warp - 2;              // 0..kV2Compute-1
     const uint32_t quad = warp & 3;            // TMEM lane quadrant
-    const uint32_t ch = cw >> 2;               // which 32 of the 64 columns
+    const uint32_t ch = cw >> 2;               // which kV2Cols of the 64 columns
     const int r = quad * 32 + lane;            // kv row of S^T / dP^T
     const uint32_t lane_addr = (quad * 32u) << 16;
     const int kv_pos = kv0 + r;
     const float sl2 = p.scale_log2;
-    const int ctid = cw * 32 + lane;           // 0..255
+    const int ctid = cw * 32 + lane;
     // statistics of query tile `it`: thread ctid < 128 owns lse row ctid, others delta
     auto load_stat = [&](int it) -> float {
       const int t = ctid & 127;
@@ -600,7 +605,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     auto half = [&](auto diag_c, int it, int h) {
       constexpr bool kDiag = decltype(diag_c)::value;
       const int buf = it & 1;
-      const int c0 = h * 64 + ch * 32;  // query column offset inside the 128-row tile
+      const int c0 = h * 64 + ch * kV2Cols;  // query column offset inside the 128-row tile
       const float* ls = lse_s + buf * 128 + c0;
       const float* dl = delta_s + buf * 128 + c0;
       mbar_wait(s_full + h, it & 1);
@@ -611,16 +616,21 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         if (lane == 0) mbar_arrive(p_ready + h);
         return;
       }
-      uint32_t sr[32], dr[32];
-      tmem_ld32(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, sr);
-      tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, dr);
+      uint32_t sr[kV2Cols], dr[kV2Cols];
+      if (kV2Cols == 32) {
+        tmem_ld32(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(dr));
+      } else {
+        tmem_ld16(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, *reinterpret_cast<uint32_t(*)[16]>(sr));
+        tmem_ld16(tmem + lane_addr + kV2ColDP + h * 64 + ch * 16, *reinterpret_cast<uint32_t(*)[16]>(dr));
+      }
       tmem_ld_wait();
-      uint32_t pk[16], dk[16];
+      uint32_t pk[kV2Cols / 2], dk[kV2Cols / 2];
       const uint64_t sl2x2 = f2(sl2, sl2);
       const uint64_t* nls2 = reinterpret_cast<const uint64_t*>(ls);  // -lse*log2e pairs
       const uint64_t* dl2 = reinterpret_cast<const uint64_t*>(dl);
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
+      for (int i = 0; i < kV2Cols; i += 2) {
         const uint64_t x2 =
             ffma2(f2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sl2x2, nls2[i / 2]);
         float x0, x1;
@@ -637,12 +647,15 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         pk[i / 2] = pack_bf16(p0, p1);
         dk[i / 2] = pack_bf16(d0, d1);
       }
-      tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 48, pk);  // own S columns
-      // dS^T row r, query columns [ch*32, ch*32+32) of this half: 16-byte chunks 4ch+v
+      if (kV2Cols == 32)  // own S columns
+        tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+      else
+        tmem_st8(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, *reinterpret_cast<const uint32_t(*)[8]>(pk));
+      // dS^T row r, query columns [ch*kV2Cols, +kV2Cols) of this half: 16-byte chunks
       uint8_t* row = smem + L::kDS + h * 16384 + r * 128;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int chunk = (4 * (int)ch + v) ^ (r & 7);
+      for (int v = 0; v < kV2Cols / 8; ++v) {
+        const int chunk = ((int)ch * (kV2Cols / 8) + v) ^ (r & 7);
         *reinterpret_cast<uint4*>(row + chunk * 16) =
             make_uint4(dk[4 * v], dk[4 * v + 1], dk[4 * v + 2], dk[4 * v + 3]);
       }
@@ -652,10 +665,13 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready + h);
     };
-    float stat = n_it > 0 ? load_stat(0) : 0.f;
+    const bool stat_thread = ctid < 256;
+    float stat = (n_it > 0 && stat_thread) ? load_stat(0) : 0.f;
     for (int it = 0; it < n_it; ++it) {
-      (ctid < 128 ? lse_s : delta_s)[(it & 1) * 128 + (ctid & 127)] = stat;
-      if (it + 1 < n_it) stat = load_stat(it + 1);  // latency hidden behind this tile
+      if (stat_thread) {
+        (ctid < 128 ? lse_s : delta_s)[(it & 1) * 128 + (ctid & 127)] = stat;
+        if (it + 1 < n_it) stat = load_stat(it + 1);  // latency hidden behind this tile
+      }
       named_bar_sync(1, 32 * kV2Compute);
       if (it == 0) {
         half(std::true_type{}, it, 0);
@@ -665,7 +681,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         half(std::false_type{}, it, 1);
       }
     }
-    // ---- epilogue: this thread writes D/2 columns of dK (scaled) and dV for kv row r
+    // ---- epilogue: this thread writes D/kCW columns of dK (scaled) and dV for kv row r
     if (n_u > 0) mbar_wait(acc_done, 0);  // all MMAs done
     tc_fence_after();
     {
@@ -673,7 +689,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       __nv_bfloat16* dk_row = p.dk + (int64_t)(seq_start + kv_pos) * p.dk_stride + (int64_t)head * D;
       __nv_bfloat16* dv_row = p.dv + (int64_t)(seq_start + kv_pos) * p.dv_stride + (int64_t)head * D;
 #pragma unroll
-      for (int c = ch * 64; c < ch * 64 + 64; c += 32) {
+      constexpr int kEpi = D / (kV2Compute / 4);  // dK/dV columns per compute thread
+      for (int c = ch * kEpi; c < ch * kEpi + kEpi; c += 32) {
         uint32_t a[32], b[32];
         tmem_ld32(tmem + lane_addr + kColDK + c, a);
         tmem_ld32(tmem + lane_addr + kColDV + c, b);
