@@ -41,7 +41,7 @@ extern "C" {
 #define FSP_ERR_CUDA (-2)
 #define FSP_ERR_UNSUPPORTED (-3)
 
-#define FSP_ABI_VERSION 1
+#define FSP_ABI_VERSION 2
 
 int fsp_abi_version(void);
 const char* fsp_last_error(void);
@@ -114,7 +114,10 @@ typedef struct FspAttnFwd {
   void* o;
   float* lse;
   int64_t q_stride, k_stride, v_stride, o_stride;
-  const int32_t* d_cu_seqlens; /* [n_seq+1], int32, device */
+  const int32_t* d_cu_seqlens; /* [n_seq+1], int32, device: lengths as prefix sums */
+  const int32_t* d_seq_starts; /* optional [n_seq] first row of each sequence (NULL: the
+                                  cu_seqlens offsets), so sequences can be read in place
+                                  from any row order that keeps each one contiguous */
   const int32_t* d_tiles;      /* schedule from fsp_attn_schedule, device */
   int32_t n_tiles;
   int32_t n_seq;
@@ -138,6 +141,7 @@ typedef struct FspAttnBwd {
   float* dq_accum;    /* workspace fp32 [n_heads, total_rows, head_dim] */
   float* delta;       /* workspace fp32 [n_heads, total_rows] */
   const int32_t* d_cu_seqlens;
+  const int32_t* d_seq_starts; /* optional, as in FspAttnFwd */
   const int32_t* d_tiles; /* kv-tile schedule (same format as forward) */
   int32_t n_tiles;
   int32_t n_seq;

@@ -42,8 +42,8 @@ class FspA2A(ctypes.Structure):
 class FspAttnFwd(ctypes.Structure):
     _fields_ = [("q", c_vp), ("k", c_vp), ("v", c_vp), ("o", c_vp), ("lse", c_vp),
                 ("q_stride", c_i64), ("k_stride", c_i64), ("v_stride", c_i64),
-                ("o_stride", c_i64), ("d_cu_seqlens", c_vp), ("d_tiles", c_vp),
-                ("n_tiles", c_i32), ("n_seq", c_i32), ("total_rows", c_i32),
+                ("o_stride", c_i64), ("d_cu_seqlens", c_vp), ("d_seq_starts", c_vp),
+                ("d_tiles", c_vp), ("n_tiles", c_i32), ("n_seq", c_i32), ("total_rows", c_i32),
                 ("n_heads", c_i32), ("head_dim", c_i32), ("softmax_scale", c_float)]
 
 
@@ -53,7 +53,7 @@ class FspAttnBwd(ctypes.Structure):
                 ("q_stride", c_i64), ("k_stride", c_i64), ("v_stride", c_i64),
                 ("o_stride", c_i64), ("do_stride", c_i64), ("dq_stride", c_i64),
                 ("dk_stride", c_i64), ("dv_stride", c_i64), ("dq_accum", c_vp),
-                ("delta", c_vp), ("d_cu_seqlens", c_vp), ("d_tiles", c_vp),
+                ("delta", c_vp), ("d_cu_seqlens", c_vp), ("d_seq_starts", c_vp), ("d_tiles", c_vp),
                 ("n_tiles", c_i32), ("n_seq", c_i32), ("total_rows", c_i32),
                 ("n_heads", c_i32), ("head_dim", c_i32), ("softmax_scale", c_float)]
 
@@ -92,7 +92,7 @@ def load() -> ctypes.CDLL:
     for name in EXPORTED:
         if not hasattr(lib, name):
             raise FspError(f"{path} does not export {name}")
-    if lib.fsp_abi_version() != 1:
+    if lib.fsp_abi_version() != 2:
         raise FspError("ABI version mismatch")
     _lib = lib
     return lib

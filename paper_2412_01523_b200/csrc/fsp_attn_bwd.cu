@@ -44,6 +44,7 @@ struct BwdParams {
   const float* delta;
   int64_t dk_stride, dv_stride;
   const int32_t* cu_seqlens;
+  const int32_t* seq_starts;  // optional: row of each sequence (else cu_seqlens)
   const int32_t* tiles;
   int32_t total_rows;
   int32_t n_heads;
@@ -96,8 +97,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int head = p.tiles[2 * blockIdx.x + 1];
   const int seq = tile >> 16;
   const int kt = tile & 0xFFFF;
-  const int seq_start = p.cu_seqlens[seq];
-  const int seqlen = p.cu_seqlens[seq + 1] - seq_start;
+  const int seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
+  const int seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
   const int kv0 = kt * kTile;
   const int nq = (seqlen + kTile - 1) / kTile;
   const int n_it = nq - kt;  // query tiles kt .. nq-1
@@ -449,8 +450,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   const int head = p.tiles[2 * blockIdx.x + 1];
   const int seq = tile >> 16;
   const int kt = tile & 0xFFFF;
-  const int seq_start = p.cu_seqlens[seq];
-  const int seqlen = p.cu_seqlens[seq + 1] - seq_start;
+  const int seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
+  const int seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
   const int kv0 = kt * kTile;
   const int nq = (seqlen + kTile - 1) / kTile;
   const int n_it = nq - kt;
@@ -792,6 +793,7 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     p.dk_stride = a->dk_stride;
     p.dv_stride = a->dv_stride;
     p.cu_seqlens = a->d_cu_seqlens;
+    p.seq_starts = a->d_seq_starts;
     p.tiles = a->d_tiles;
     p.total_rows = T;
     p.n_heads = H;

@@ -31,6 +31,7 @@ struct FwdParams {
   float* lse;
   int64_t o_stride;
   const int32_t* cu_seqlens;
+  const int32_t* seq_starts;  // optional: row of each sequence (else cu_seqlens)
   const int32_t* tiles;
   int32_t total_rows;
   int32_t n_heads;
@@ -73,8 +74,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int head = p.tiles[2 * blockIdx.x + 1];
   const int seq = tile >> 16;
   const int qt = tile & 0xFFFF;
-  const int seq_start = p.cu_seqlens[seq];
-  const int seqlen = p.cu_seqlens[seq + 1] - seq_start;
+  const int seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
+  const int seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
   const int q0 = qt * kBM;
   const int n_kv = qt + 1;  // causal: kv tiles 0..qt (kBM == kBN)
 
@@ -349,8 +350,8 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   const int head = p.tiles[2 * blockIdx.x + 1];
   const int seq = tile >> 16;
   const int pair = tile & 0xFFFF;
-  const int seq_start = p.cu_seqlens[seq];
-  const int seqlen = p.cu_seqlens[seq + 1] - seq_start;
+  const int seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
+  const int seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
   const int q0 = pair * 256;
   const bool has_b = q0 + 128 < seqlen;
   const int n_a = 2 * pair + 1;                 // kv tiles seen by tile A (causal)
@@ -682,6 +683,7 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   p.lse = a->lse;
   p.o_stride = a->o_stride;
   p.cu_seqlens = a->d_cu_seqlens;
+  p.seq_starts = a->d_seq_starts;
   p.tiles = a->d_tiles;
   p.total_rows = a->total_rows;
   p.n_heads = a->n_heads;

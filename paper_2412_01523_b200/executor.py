@@ -83,6 +83,7 @@ class RankMicroBatch:
     unpack_table: torch.Tensor | None = None  # int32 [d*R]
     sched: ops.AttnSchedule | None = None
     fwd_flops: float = 0.0                  # 2 * D * (H/d) * sum s^2 (causal, FA convention)
+    in_place: bool = False                  # d = 1: attention runs on the loader-order rows
 
 
 @dataclass
@@ -135,10 +136,22 @@ class FlexSPExecutor:
                 rmb.pack_index = torch.from_numpy(grp.pack_index(j)).to(self.device)
                 rmb.unpack_table = torch.from_numpy(
                     np.ascontiguousarray(grp.unpack_table().reshape(-1))).to(self.device)
-                rmb.sched = ops.AttnSchedule.build(grp.cu_seqlens, self.device,
-                                                   self.n_heads // grp.degree,
-                                                   total_rows=grp.padded_tokens,
-                                                   head_dim=self.head_dim)
+                if grp.degree == 1:
+                    # d = 1: no exchange at all — attention reads q/k/v and writes O / dQKV
+                    # in place in the rank's loader-order buffers (each sequence is
+                    # contiguous there), so there is no pack / unpack copy either.
+                    offs = np.zeros(len(lengths) + 1, dtype=np.int64)
+                    np.cumsum(np.asarray(lengths, dtype=np.int64), out=offs[1:])
+                    starts = np.searchsorted(local, offs[list(grp.sequence_indices)])
+                    rmb.sched = ops.AttnSchedule.build(
+                        grp.cu_seqlens, self.device, self.n_heads, total_rows=rmb.n_local,
+                        head_dim=self.head_dim, seq_starts_host=starts)
+                    rmb.in_place = True
+                else:
+                    rmb.sched = ops.AttnSchedule.build(grp.cu_seqlens, self.device,
+                                                       self.n_heads // grp.degree,
+                                                       total_rows=grp.padded_tokens,
+                                                       head_dim=self.head_dim)
                 seg = np.diff(grp.cu_seqlens).astype(np.float64)
                 rmb.fwd_flops = 2.0 * self.head_dim * (self.n_heads // grp.degree) * float((seg ** 2).sum())
                 mbs.append(rmb)
@@ -212,6 +225,14 @@ class FlexSPExecutor:
         ranks = grp.ranks
         if qkv_local.shape[0] != mb.n_local:
             raise ValueError(f"rank {self.rank} expects {mb.n_local} local rows, got {qkv_local.shape[0]}")
+        if mb.in_place:
+            for _ in range(2):  # keep the barrier epochs in step with the exchanging ranks
+                self._next_epoch()
+            out_local, _ = self.local_buffers(sp, mb)
+            with self.timer.span("attn_fwd", mb.fwd_flops):
+                _, lse = ops.attn_fwd(qkv_local[:, 0], qkv_local[:, 1], qkv_local[:, 2], mb.sched,
+                                      self.scale, out=out_local)
+            return out_local, (qkv_local, out_local, lse)
         off = sp.offsets
         recv = self.heap.view(off["qkv_recv"], (grp.padded_tokens, 3, hs, D), torch.bfloat16)
         sent = float((d - 1) * R * hs * D * 2)  # NVLink bytes this rank sends per matrix
@@ -250,6 +271,18 @@ class FlexSPExecutor:
             return None
         recv, o_heads, lse = saved
         H, D = self.n_heads, self.head_dim
+        if mb.in_place:
+            for _ in range(2):
+                self._next_epoch()
+            _, dqkv_local = self.local_buffers(sp, mb)
+            T = mb.n_local
+            dq_acc = self._workspace("dq_accum", T * H * D, torch.float32)
+            delta = self._workspace("delta", H * T, torch.float32)
+            with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
+                ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, dout_local, lse,
+                             mb.sched, self.scale, dq=dqkv_local[:, 0], dk=dqkv_local[:, 1],
+                             dv=dqkv_local[:, 2], dq_accum=dq_acc, delta=delta)
+            return dqkv_local
         d, j, R = grp.degree, mb.j, grp.rows_per_rank
         hs = H // d
         ranks = grp.ranks

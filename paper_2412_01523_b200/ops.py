@@ -69,6 +69,7 @@ class AttnSchedule:
     head_dim: int
     total_rows: int
     max_seqlen: int
+    seq_starts: torch.Tensor | None = None  # int32 [n_seq] device, None = cu_seqlens offsets
 
     @property
     def n_fwd(self) -> int:
@@ -80,8 +81,12 @@ class AttnSchedule:
 
     @staticmethod
     def build(cu_seqlens_host, device, n_heads: int, total_rows: int | None = None,
-              head_dim: int = 128) -> "AttnSchedule":
-        """`total_rows` >= cu[-1] lets the packed buffer carry trailing pad rows."""
+              head_dim: int = 128, seq_starts_host=None) -> "AttnSchedule":
+        """`total_rows` >= cu[-1] lets the packed buffer carry trailing pad rows.
+
+        `seq_starts_host` (optional) gives the first row of every sequence when the
+        sequences sit in place in some other contiguous-per-sequence row order (e.g. a
+        rank's loader-order buffer), so no pack / unpack copy is needed."""
         cu = np.ascontiguousarray(np.asarray(cu_seqlens_host, dtype=np.int32))
         n_seq = len(cu) - 1
         rows = int(cu[-1]) if total_rows is None else int(total_rows)
@@ -101,8 +106,14 @@ class AttnSchedule:
                 capi.check(got)
             tiles.append(torch.from_numpy(buf[:2 * n].copy()).to(device))
         lens = np.diff(cu)
+        starts = None
+        if seq_starts_host is not None:
+            st = np.ascontiguousarray(np.asarray(seq_starts_host, dtype=np.int64))
+            if st.shape != (n_seq,) or (n_seq and (st.min() < 0 or (st + lens).max() > rows)):
+                raise ValueError("seq_starts must give one in-range start row per sequence")
+            starts = torch.from_numpy(st.astype(np.int32)).to(device)
         return AttnSchedule(torch.from_numpy(cu.copy()).to(device), tiles[0], tiles[1], n_seq,
-                            n_heads, head_dim, rows, int(lens.max()) if n_seq else 0)
+                            n_heads, head_dim, rows, int(lens.max()) if n_seq else 0, starts)
 
 
 def _rows_view_ok(t: torch.Tensor, H: int, D: int) -> None:
@@ -127,7 +138,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
     lse = torch.empty((H, T), dtype=torch.float32, device=q.device)
     a = capi.FspAttnFwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
                         q.stride(0), k.stride(0), v.stride(0), o.stride(0),
-                        sched.cu_seqlens.data_ptr(), sched.fwd_tiles.data_ptr(),
+                        sched.cu_seqlens.data_ptr(), _ptr(sched.seq_starts), sched.fwd_tiles.data_ptr(),
                         sched.n_fwd, sched.n_seq, T, H, D, scale)
     capi.check(capi.load().fsp_attn_fwd(ctypes.byref(a), _stream()))
     LAUNCHES[0] += 1 if sched.n_fwd else 0
@@ -161,7 +172,8 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
                         lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
                         q.stride(0), k.stride(0), v.stride(0), o.stride(0), dout.stride(0),
                         dq.stride(0), dk.stride(0), dv.stride(0), dq_acc.data_ptr(),
-                        delta.data_ptr(), sched.cu_seqlens.data_ptr(), sched.bwd_tiles.data_ptr(),
+                        delta.data_ptr(), sched.cu_seqlens.data_ptr(), _ptr(sched.seq_starts),
+                        sched.bwd_tiles.data_ptr(),
                         sched.n_bwd, sched.n_seq, T, H, D, scale)
     capi.check(capi.load().fsp_attn_bwd(ctypes.byref(a), _stream()))
     LAUNCHES[0] += (2 if T else 0) + (1 if sched.n_bwd else 0)
