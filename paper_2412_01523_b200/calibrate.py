@@ -1,0 +1,87 @@
+"""B200 profiler -> ProfileRecord CSV -> fitted planner coefficients.
+
+The reference planner prices a group of degree d holding lengths s_k as
+    comp = (1/d) Σ(α1 s² + α2 s) + β1,  comm = (1/(d v)) Σ α3 s + β2,
+    mem  = (Σ s / d) m_token + m_ms                       (pkg/src/seqplan/cost_model.py:1-12)
+and fits α/β/m from profile records (cost_model.py:181-244) read from a semicolon CSV
+`tokens;degree;bandwidth;comp_s;comm_s;mem_bytes` (cost_model.py:247-295,
+pkg/docs/formats.md:62-72).  This module produces those records from the SP step running
+on B200: each record is one group executed by FlexSPExecutor, with compute time = the
+group's attention fwd+bwd CUDA-event time (max over its ranks), comm time = its all-to-all
++ barrier time, and memory = the bytes the step allocates per device for that group.
+The fit itself is the reference's own `fit_coefficients` (imported, not re-implemented).
+"""
+from __future__ import annotations
+
+import csv
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+PROFILE_HEADER = ["tokens", "degree", "bandwidth", "comp_s", "comm_s", "mem_bytes"]
+
+
+@dataclass(frozen=True)
+class GroupMeasurement:
+    token_lengths: tuple[int, ...]
+    degree: int
+    bandwidth: float
+    comp_s: float
+    comm_s: float
+    mem_bytes: float
+
+
+def write_profile_csv(path, rows: Sequence[GroupMeasurement]) -> None:
+    """Same layout as seqplan.cost_model.write_profile_csv (cost_model.py:283-295)."""
+    with open(path, "w", newline="", encoding="utf-8") as fh:
+        w = csv.writer(fh, delimiter=";", lineterminator="\n")
+        w.writerow(PROFILE_HEADER)
+        for r in rows:
+            w.writerow([",".join(str(int(s)) for s in r.token_lengths), r.degree, r.bandwidth,
+                        r.comp_s, r.comm_s, r.mem_bytes])
+
+
+def step_bytes_per_device(lengths: Sequence[int], degree: int, n_heads: int, head_dim: int) -> float:
+    """Device bytes one rank of a degree-d group allocates for the attention-layer step:
+    loader-order q/k/v, dO, O, dQKV (bf16) of its shard, plus — for d > 1 — the
+    head-sharded exchange buffers (q/k/v, dO, O, dQKV over the whole group), and the fp32
+    softmax statistics / dQ accumulator of its head slice."""
+    t = int(sum(lengths))
+    t_pad = -(-t // degree) * degree
+    h = n_heads * head_dim
+    shard = t_pad // degree
+    b = shard * (3 + 1 + 1 + 3) * h * 2
+    hs = h // degree
+    if degree > 1:
+        b += t_pad * (3 + 1 + 1 + 3) * hs * 2
+    b += t_pad * hs * 4 + 2 * t_pad * (n_heads // degree) * 4  # dq_accum, lse, delta
+    return float(b)
+
+
+def fit(rows: Sequence[GroupMeasurement], allow_underdetermined: bool = False):
+    """Fit planner coefficients with the reference's own least squares."""
+    from seqplan.cost_model import ProfileRecord, fit_coefficients
+    recs = [ProfileRecord(tuple(int(s) for s in r.token_lengths), r.degree, r.bandwidth,
+                          r.comp_s, r.comm_s, r.mem_bytes) for r in rows]
+    return fit_coefficients(recs, allow_underdetermined=allow_underdetermined)
+
+
+def group_loads(lengths: Sequence[int], degrees: Sequence[int], per_degree: int, seed: int = 0):
+    """Deterministic spread of group loads: for each degree, `per_degree` subsets of the batch
+    with distinct token totals (short-only, long-only and mixed)."""
+    rng = np.random.default_rng(seed)
+    order = np.argsort(np.asarray(lengths))
+    out = []
+    for d in degrees:
+        for i in range(per_degree):
+            frac = (i + 1) / (per_degree + 1)
+            k = max(1, int(round(frac * len(lengths))))
+            if i % 3 == 0:
+                pick = order[:k]                       # shortest k
+            elif i % 3 == 1:
+                pick = order[-max(1, k // 4):]         # a few of the longest
+            else:
+                pick = rng.choice(len(lengths), size=k, replace=False)
+            out.append((int(d), [int(lengths[j]) for j in sorted(pick.tolist())]))
+    return out
