@@ -60,11 +60,25 @@ def step_bytes_per_device(lengths: Sequence[int], degree: int, n_heads: int, hea
 
 
 def fit(rows: Sequence[GroupMeasurement], allow_underdetermined: bool = False):
-    """Fit planner coefficients with the reference's own least squares."""
+    """Fit planner coefficients with the reference's own least squares.
+
+    d = 1 groups exchange nothing, so they measure comm = 0 exactly; the reference weights
+    residuals by 1/|measurement| (cost_model.py:94-104), which would pin α3, β2 to zero on
+    those rows.  The communication channel is therefore fitted on the d >= 2 records only
+    (a second call of the same reference routine) and merged with the compute/memory fit
+    of all records.  Returns (FitResult of all records, CostCoefficients merged)."""
     from seqplan.cost_model import ProfileRecord, fit_coefficients
+    from seqplan.domain import CostCoefficients
     recs = [ProfileRecord(tuple(int(s) for s in r.token_lengths), r.degree, r.bandwidth,
                           r.comp_s, r.comm_s, r.mem_bytes) for r in rows]
-    return fit_coefficients(recs, allow_underdetermined=allow_underdetermined)
+    full = fit_coefficients(recs, allow_underdetermined=allow_underdetermined)
+    multi = [r for r in recs if r.degree > 1]
+    c = full.coefficients
+    if multi:
+        comm = fit_coefficients(multi, allow_underdetermined=True).coefficients
+        c = CostCoefficients(alpha1=c.alpha1, alpha2=c.alpha2, beta1=c.beta1, alpha3=comm.alpha3,
+                             beta2=comm.beta2, m_token=c.m_token, m_ms=c.m_ms)
+    return full, c
 
 
 def group_loads(lengths: Sequence[int], degrees: Sequence[int], per_degree: int, seed: int = 0):
@@ -85,3 +99,16 @@ def group_loads(lengths: Sequence[int], degrees: Sequence[int], per_degree: int,
                 pick = rng.choice(len(lengths), size=k, replace=False)
             out.append((int(d), [int(lengths[j]) for j in sorted(pick.tolist())]))
     return out
+
+
+def predict(coeffs, rows: Sequence[GroupMeasurement]) -> dict:
+    """Model predictions for the profiled groups and the max relative errors."""
+    comp_err = comm_err = 0.0
+    for r in rows:
+        lens = r.token_lengths
+        comp = sum(coeffs.alpha1 * s * s + coeffs.alpha2 * s for s in lens) / r.degree + coeffs.beta1
+        comm = sum(coeffs.alpha3 * s for s in lens) / (r.degree * r.bandwidth) + coeffs.beta2
+        comp_err = max(comp_err, abs(comp - r.comp_s) / max(r.comp_s, 1e-12))
+        if r.degree > 1:
+            comm_err = max(comm_err, abs(comm - r.comm_s) / max(r.comm_s, 1e-12))
+    return {"comp_rel_error": comp_err, "comm_rel_error_d_ge_2": comm_err}

@@ -85,10 +85,11 @@ def main():
         calibrate.write_profile_csv(args.out + ".csv", rows)
         result = {"records": len(rows), "degrees": degrees, "world": world}
         try:
-            fr = calibrate.fit(rows, allow_underdetermined=len(degrees) < 2)
-            result.update({"coefficients": fr.coefficients.to_json_dict(),
-                           "max_rel_error": fr.max_rel_error, "comp_rel_error": fr.comp_rel_error,
-                           "comm_rel_error": fr.comm_rel_error, "mem_rel_error": fr.mem_rel_error,
+            fr, merged = calibrate.fit(rows, allow_underdetermined=len(degrees) < 2)
+            pred = calibrate.predict(merged, rows)
+            result.update({"coefficients": merged.to_json_dict(),
+                           "comp_rel_error": fr.comp_rel_error, "mem_rel_error": fr.mem_rel_error,
+                           "comm_rel_error_d_ge_2": pred["comm_rel_error_d_ge_2"],
                            "clamped": list(fr.clamped), "warnings": list(fr.warnings)})
         except ImportError as exc:  # reference package not shipped to this box
             result["fit"] = f"skipped: {exc}"

@@ -44,11 +44,13 @@ def test_fit_recovers_coefficients():
              "beta2": 3e-5, "m_token": 2e5, "m_ms": 2e9}
     lengths = [1024 + 37 * i * i for i in range(40)]
     loads = calibrate.group_loads(lengths, [1, 2, 4], per_degree=5)
-    fr = calibrate.fit(_synthetic(truth, loads))
-    got = fr.coefficients.to_json_dict()
+    fr, merged = calibrate.fit(_synthetic(truth, loads))
+    got = merged.to_json_dict()
     for k, v in truth.items():
         assert got[k] == pytest.approx(v, rel=1e-6), k
-    assert fr.max_rel_error < 1e-9
+    assert fr.comp_rel_error < 1e-9
+    pred = calibrate.predict(merged, _synthetic(truth, loads))
+    assert pred["comm_rel_error_d_ge_2"] < 1e-9
 
 
 def test_group_loads_are_deterministic_and_distinct():
