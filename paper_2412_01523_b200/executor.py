@@ -189,9 +189,11 @@ class FlexSPExecutor:
     def _signals(self, ranks: range) -> list[int]:
         return [self.heap.peer(r, 0) for r in ranks]
 
-    def _barrier(self, ranks: range, epoch: int) -> None:
+    def _barrier(self, ranks: range, epoch: int, span: str = "group_barrier") -> None:
         if len(ranks) > 1:
-            ops.group_barrier(self._signals(ranks), self.rank - ranks.start, ranks.start, epoch)
+            with self.timer.span(span):
+                ops.group_barrier(self._signals(ranks), self.rank - ranks.start, ranks.start,
+                                  epoch)
 
     def _next_epoch(self) -> int:
         self.epoch += 1
@@ -213,7 +215,7 @@ class FlexSPExecutor:
 
         Returns (out_local view [n_local, H, D], saved) where saved feeds the backward.
         """
-        self._barrier(range(self.world_size), self._next_epoch())  # regroup point
+        self._barrier(range(self.world_size), self._next_epoch(), "world_barrier")  # regroup
         grp = mb.group
         if grp is None:
             for _ in range(2):
