@@ -19,6 +19,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 from oracle.attention_ref import attention_bwd_ref, attention_fwd_ref  # noqa: E402
+from paper_2412_01523_b200.attention import FlexSPAttention  # noqa: E402
 from paper_2412_01523_b200.executor import FlexSPExecutor  # noqa: E402
 
 DEFAULT = {2: "c1_flexsp_2tier.json", 4: "rand0_n4_flexsp.json", 8: "rand1_n8_flexsp.json"}
@@ -54,6 +55,24 @@ def main():
         got.clear()
         ex.step(sp, ins, dos, sink=sink)
     torch.cuda.synchronize()
+    # the same micro-batches through the autograd Function, all forwards before any
+    # backward: outputs and dK/dV must equal the executor step's bit for bit on every rank
+    leaves, outs = {}, {}
+    for m in range(len(sp.micro_batches)):
+        leaves[m] = ins[m].clone().requires_grad_(True)
+        outs[m] = FlexSPAttention.apply(leaves[m], ex, sp, m)
+    for m in reversed(range(len(sp.micro_batches))):
+        outs[m].backward(dos[m])
+    torch.cuda.synchronize()
+    autograd_ok = True
+    for m, (_, out, dqkv) in got.items():
+        g_ = leaves[m].grad.float().cpu()
+        autograd_ok = autograd_ok and torch.equal(outs[m].detach().float().cpu(), out) and \
+            torch.equal(g_[:, 1:], dqkv[:, 1:]) and \
+            bool(torch.allclose(g_[:, 0], dqkv[:, 0], atol=1e-2, rtol=1e-2))
+    flag_ag = torch.tensor([1 if autograd_ok else 0], device=dev)
+    dist.all_reduce(flag_ag, op=dist.ReduceOp.MIN)
+    autograd_ok = bool(flag_ag.item())
     parts = [None] * world
     dist.all_gather_object(parts, got)
     ok = True
@@ -69,7 +88,8 @@ def main():
         o_ref, _ = attention_fwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], cu)
         refs = attention_bwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], dout, cu)
         e_o = (o - o_ref).abs()
-        ok = bool(torch.isfinite(o).all()) and e_o.max() <= 2e-2 and e_o.mean() <= 2e-3
+        ok = autograd_ok and bool(torch.isfinite(o).all()) and e_o.max() <= 2e-2 and \
+            e_o.mean() <= 2e-3
         errs = []
         for i, r in enumerate(refs):
             e = (dq[:, i] - r).abs()
@@ -80,7 +100,7 @@ def main():
                 for mb in plan["micro_batches"]]
         print(json.dumps({"plan": name, "world": world, "groups": degs, "tokens": T,
                           "o_max": float(e_o.max()), "o_mean": float(e_o.mean()),
-                          "grad_max": errs, "ok": ok}), flush=True)
+                          "grad_max": errs, "autograd_ok": autograd_ok, "ok": ok}), flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, 0)
     dist.destroy_process_group()

@@ -178,3 +178,42 @@ def test_step_from_host_matches_device_step():
     for m in range(len(toks)):
         torch.testing.assert_close(res[("host", m)][0], res[("dev", m)][0])
         torch.testing.assert_close(res[("host", m)][1], res[("dev", m)][1], atol=2e-2, rtol=2e-2)
+
+
+def test_flexsp_attention_autograd_two_layers():
+    """FlexSPAttention.apply through torch autograd: two layers' forwards of every
+    micro-batch run before any backward (so the heap regions are reused in between), and
+    outputs and dK/dV equal the executor's own step bit for bit (dQ to fp32 reduction order)."""
+    from paper_2412_01523_b200.attention import FlexSPAttention
+    from paper_2412_01523_b200.executor import FlexSPExecutor
+    H, D = 4, 128
+    lengths = [700, 1, 130, 2048, 64, 300]
+    plan = _plan_n1(lengths, [[3, 1, 5], [0, 2, 4]])
+    ex = FlexSPExecutor(1, 0, H, D, "cuda")
+    sp = ex.prepare(plan, lengths)
+    g = torch.Generator().manual_seed(11)
+    toks = [torch.from_numpy(mb.local_tokens) for mb in sp.micro_batches]
+    T = sum(lengths)
+    layers = [(torch.randn(T, 3, H, D, generator=g).bfloat16(), torch.randn(T, H, D, generator=g).bfloat16())
+              for _ in range(2)]
+    ref = {}
+    for li, (qkv, dout) in enumerate(layers):
+        def sink(m, out, dqkv, li=li):
+            ref[(li, m)] = (out.clone(), dqkv.clone())
+        ex.step(sp, [qkv[t].cuda() for t in toks], [dout[t].cuda() for t in toks], sink=sink)
+    leaves, outs = {}, {}
+    for m, t in enumerate(toks):
+        for li, (qkv, _) in enumerate(layers):
+            x = qkv[t].cuda().requires_grad_(True)
+            leaves[(li, m)] = x
+            outs[(li, m)] = FlexSPAttention.apply(x, ex, sp, m)
+    for m in reversed(range(len(toks))):
+        for li in reversed(range(2)):
+            outs[(li, m)].backward(layers[li][1][toks[m]].cuda())
+    torch.cuda.synchronize()
+    for key, (o_ref, d_ref) in ref.items():
+        assert torch.equal(outs[key].detach(), o_ref), key
+        grad = leaves[key].grad
+        assert torch.equal(grad[:, 1:], d_ref[:, 1:]), key  # dK, dV: one writer per row
+        # dQ sums fp32 reductions from several CTAs in whatever order they land
+        torch.testing.assert_close(grad[:, 0].float(), d_ref[:, 0].float(), atol=1e-2, rtol=1e-2)
