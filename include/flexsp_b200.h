@@ -41,7 +41,7 @@ extern "C" {
 #define FSP_ERR_CUDA (-2)
 #define FSP_ERR_UNSUPPORTED (-3)
 
-#define FSP_ABI_VERSION 2
+#define FSP_ABI_VERSION 3
 
 int fsp_abi_version(void);
 const char* fsp_last_error(void);
@@ -72,16 +72,23 @@ int fsp_unpack_rows(const void* src, int64_t src_stride_bytes, void* dst, int64_
  *   non-null the unpack is fused: d_dst_index is [degree][R] — the unpack tables of all
  *   group members — and shard row i of member j lands in its destination row
  *   d_dst_index[j*R + i] (negative -> dropped, i.e. a pad row).
+ *
+ * Uneven heads (ABI 3): when head_begin[degree] != 0, member j owns heads
+ *   [head_begin[j], head_begin[j+1]) (e.g. 52 heads at d=8: 7,7,7,7,6,6,6,6 — the 30B
+ *   shape) instead of [j*H/d, (j+1)*H/d).  The head-sharded side then
+ *   spaces its n_mats matrices hmax*D elements apart, hmax = max_j of the head counts
+ *   (member j uses the first H_j heads of each); all zero = the even split.
  */
 typedef struct FspA2A {
   int32_t degree;        /* d, power of two, 1..8 */
   int32_t rank;          /* rank inside the group, 0..d-1 */
   int32_t rows_per_rank; /* R = T_g / d (T_g padded to a multiple of d) */
   int32_t n_mats;        /* 3 for q,k,v; 1 for o / do */
-  int32_t n_heads;       /* H (total, divisible by d) */
+  int32_t n_heads;       /* H (total; divisible by d unless head_begin is set) */
   int32_t head_dim;      /* D */
   int64_t src_stride;    /* elements between consecutive source rows */
   int64_t dst_stride;    /* elements between consecutive destination rows */
+  int32_t head_begin[9]; /* optional uneven split: prefix offsets, [0..degree]; zeros = even */
 } FspA2A;
 
 int fsp_a2a_seq2head(const FspA2A* a, const void* src, void* const* peer_dst,

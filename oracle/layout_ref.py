@@ -103,19 +103,31 @@ def microbatch_tables(micro_batch, lengths, world_size):
     return out
 
 
+def head_split(n_heads, d):
+    """Head ranges of the d group members: member j owns heads [b[j], b[j+1]); the first
+    n_heads % d members take one extra head (52 heads at d=8 -> 7,7,7,7,6,6,6,6; the
+    even split when d divides n_heads).  SURVEY.md §7 H5; PAPER.md:1458 (30B, 52 heads)."""
+    base, extra = divmod(n_heads, d)
+    b = [0]
+    for j in range(d):
+        b.append(b[-1] + base + (1 if j < extra else 0))
+    return b
+
+
 def ulysses_seq2head(shards, n_mats, n_heads, head_dim):
-    """Eq. (2): list of d arrays [R, n_mats, H, D] -> list of d arrays [d*R, n_mats, H/d, D]."""
+    """Eq. (2): list of d arrays [R, n_mats, H, D] -> list of d arrays
+    [d*R, n_mats, H_j, D], H_j = member j's head count (head_split)."""
     d = len(shards)
-    hs = n_heads // d
+    b = head_split(n_heads, d)
     out = []
     for j in range(d):
-        parts = [sh[:, :, j * hs:(j + 1) * hs, :] for sh in shards]
+        parts = [sh[:, :, b[j]:b[j + 1], :] for sh in shards]
         out.append(np.concatenate(parts, axis=0))
     return out
 
 
 def ulysses_head2seq(heads, n_mats, n_heads, head_dim):
-    """Eq. (4): list of d arrays [d*R, n_mats, H/d, D] -> list of d arrays [R, n_mats, H, D]."""
+    """Eq. (4): list of d arrays [d*R, n_mats, H_j, D] -> list of d arrays [R, n_mats, H, D]."""
     d = len(heads)
     r = heads[0].shape[0] // d
     out = []

@@ -13,27 +13,43 @@ import torch
 import torch.distributed as dist
 
 from .attention_ref import attention_fwd_ref
+from .layout_ref import head_split
 
 
 def seq2head(shard: torch.Tensor, group=None) -> torch.Tensor:
-    """[R, n_mats, H, D] on each of d ranks -> [d*R, n_mats, H/d, D] (Eq. 2)."""
+    """[R, n_mats, H, D] on each of d ranks -> [d*R, n_mats, H_me, D] (Eq. 2); member j
+    receives heads [b[j], b[j+1]) of layout_ref.head_split (uneven when d does not
+    divide H)."""
     d = dist.get_world_size(group)
+    me = dist.get_rank(group)
     R, M, H, D = shard.shape
-    send = shard.reshape(R, M, d, H // d, D).permute(2, 0, 1, 3, 4).contiguous()
-    recv = torch.empty_like(send)
-    dist.all_to_all_single(recv, send, group=group)
-    return recv.reshape(d * R, M, H // d, D)
+    b = head_split(H, d)
+    send = torch.cat([shard[:, :, b[j]:b[j + 1]].reshape(-1) for j in range(d)])
+    h_me = b[me + 1] - b[me]
+    recv = torch.empty(d * R * M * h_me * D, dtype=shard.dtype)
+    dist.all_to_all_single(recv, send, output_split_sizes=[R * M * h_me * D] * d,
+                           input_split_sizes=[R * M * (b[j + 1] - b[j]) * D for j in range(d)],
+                           group=group)
+    return recv.reshape(d * R, M, h_me, D)
 
 
-def head2seq(heads: torch.Tensor, group=None) -> torch.Tensor:
-    """[d*R, n_mats, H/d, D] -> [R, n_mats, H, D] (Eq. 4)."""
+def head2seq(heads: torch.Tensor, group=None, n_heads: int | None = None) -> torch.Tensor:
+    """[d*R, n_mats, H_me, D] -> [R, n_mats, H, D] (Eq. 4)."""
     d = dist.get_world_size(group)
-    T, M, Hs, D = heads.shape
+    T, M, h_me, D = heads.shape
     R = T // d
-    send = heads.reshape(d, R, M, Hs, D).contiguous()
-    recv = torch.empty_like(send)
-    dist.all_to_all_single(recv, send, group=group)
-    return recv.permute(1, 2, 0, 3, 4).reshape(R, M, d * Hs, D)
+    H = n_heads if n_heads is not None else h_me * d
+    b = head_split(H, d)
+    recv = torch.empty(R * M * H * D, dtype=heads.dtype)
+    dist.all_to_all_single(recv, heads.reshape(-1).contiguous(),
+                           output_split_sizes=[R * M * (b[j + 1] - b[j]) * D for j in range(d)],
+                           input_split_sizes=[R * M * h_me * D] * d, group=group)
+    parts, off = [], 0
+    for j in range(d):
+        n = R * M * (b[j + 1] - b[j]) * D
+        parts.append(recv[off:off + n].reshape(R, M, b[j + 1] - b[j], D))
+        off += n
+    return torch.cat(parts, dim=2)
 
 
 def ulysses_attention(shard_qkv: torch.Tensor, cu_seqlens, group=None) -> torch.Tensor:
@@ -43,4 +59,4 @@ def ulysses_attention(shard_qkv: torch.Tensor, cu_seqlens, group=None) -> torch.
     o = torch.zeros(T, heads.shape[2], heads.shape[3])
     n = int(cu_seqlens[-1])
     o[:n], _ = attention_fwd_ref(heads[:n, 0], heads[:n, 1], heads[:n, 2], cu_seqlens)
-    return head2seq(o[:, None], group)[:, 0]
+    return head2seq(o[:, None], group, n_heads=shard_qkv.shape[2])[:, 0]

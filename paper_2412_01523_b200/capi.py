@@ -36,7 +36,7 @@ EXPORTED = (
 class FspA2A(ctypes.Structure):
     _fields_ = [("degree", c_i32), ("rank", c_i32), ("rows_per_rank", c_i32),
                 ("n_mats", c_i32), ("n_heads", c_i32), ("head_dim", c_i32),
-                ("src_stride", c_i64), ("dst_stride", c_i64)]
+                ("src_stride", c_i64), ("dst_stride", c_i64), ("head_begin", c_i32 * 9)]
 
 
 class FspAttnFwd(ctypes.Structure):
@@ -92,7 +92,7 @@ def load() -> ctypes.CDLL:
     for name in EXPORTED:
         if not hasattr(lib, name):
             raise FspError(f"{path} does not export {name}")
-    if lib.fsp_abi_version() != 2:
+    if lib.fsp_abi_version() != 3:
         raise FspError("ABI version mismatch")
     _lib = lib
     return lib

@@ -9,6 +9,8 @@
 // plans costs nothing.  The pack (loader-order -> group-packed rows) is fused into the
 // send by reading source rows through the permutation; the unpack is fused into the
 // receive side of head2seq the same way.
+#include <algorithm>
+
 #include "fsp_host.h"
 
 namespace fsp {
@@ -29,7 +31,7 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return r;
 }
 
-// One warp moves one (row i, matrix m, peer j) chunk = the (H/d)*D*2-byte head slice of
+// One warp moves one (row i, matrix m, peer j) chunk = the H_j*D*2-byte head slice of
 // one row (1 KB at C2/d=8): index math once per chunk, 32 lanes x 16-byte vectors with
 // kUnroll loads in flight per lane.  Peer j is the fastest-varying chunk coordinate so the
 // local copy (j == rank) and the NVLink writes to all peers proceed concurrently, and the
@@ -40,12 +42,16 @@ template <bool kSeq2Head>
 __global__ void __launch_bounds__(kThreads) a2a_kernel(const uint8_t* __restrict__ src,
                                                        PeerPtrs dst, const int32_t* __restrict__ index,
                                                        FspA2A a) {
+  // a.head_begin is normalised by the host (even split filled in): member j owns heads
+  // [head_begin[j], head_begin[j+1]); the head-sharded side spaces matrices hmax heads apart
   const int d = a.degree;
-  const int slice_bytes = (a.n_heads / d) * a.head_dim * 2;
-  const int vpc = slice_bytes >> 4;
+  int hmax = 0;
+  for (int jj = 0; jj < d; ++jj) hmax = max(hmax, a.head_begin[jj + 1] - a.head_begin[jj]);
+  const int64_t head_bytes = (int64_t)a.head_dim * 2;
+  const int64_t sharded_mat = hmax * head_bytes;  // bytes per matrix on the head-sharded side
   const uint32_t n_chunks = (uint32_t)a.rows_per_rank * (uint32_t)a.n_mats * (uint32_t)d;
   const int64_t src_stride = a.src_stride * 2, dst_stride = a.dst_stride * 2;
-  const int64_t full_row = (int64_t)a.n_heads * a.head_dim * 2;  // bytes of all heads of one mat
+  const int64_t full_row = (int64_t)a.n_heads * head_bytes;  // bytes of all heads of one mat
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (kThreads / 32);
   for (uint32_t c = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); c < n_chunks; c += warps) {
@@ -56,22 +62,27 @@ __global__ void __launch_bounds__(kThreads) a2a_kernel(const uint8_t* __restrict
     const int4* sp;
     int4* dp;
     bool zero = false;
+    int vpc;
     if (kSeq2Head) {
-      // local shard row i (all heads) -> peer j row (rank*R + i), head slice j
+      // local shard row i (all heads) -> peer j row (rank*R + i), peer j's heads
+      const int hb = a.head_begin[j];
+      vpc = (int)(((a.head_begin[j + 1] - hb) * head_bytes) >> 4);
       const int32_t srow = index ? index[i] : (int32_t)i;
       zero = srow < 0;
       sp = reinterpret_cast<const int4*>(src + (int64_t)(zero ? 0 : srow) * src_stride +
-                                         m * full_row + (int64_t)j * slice_bytes);
+                                         m * full_row + hb * head_bytes);
       const int64_t drow = (int64_t)a.rank * a.rows_per_rank + i;
-      dp = reinterpret_cast<int4*>(dst.p[j] + drow * dst_stride + (int64_t)m * slice_bytes);
+      dp = reinterpret_cast<int4*>(dst.p[j] + drow * dst_stride + (int64_t)m * sharded_mat);
     } else {
-      // local row (j*R + i), own head slice -> peer j shard row i at head slice `rank`
+      // local row (j*R + i), own heads -> peer j shard row i at this rank's head offset
+      const int hb = a.head_begin[a.rank];
+      vpc = (int)(((a.head_begin[a.rank + 1] - hb) * head_bytes) >> 4);
       const int64_t srow = (int64_t)j * a.rows_per_rank + i;
       const int32_t drow = index ? index[(int64_t)j * a.rows_per_rank + i] : (int32_t)i;
       if (drow < 0) continue;  // pad row: dropped (warp-uniform)
-      sp = reinterpret_cast<const int4*>(src + srow * src_stride + (int64_t)m * slice_bytes);
+      sp = reinterpret_cast<const int4*>(src + srow * src_stride + (int64_t)m * sharded_mat);
       dp = reinterpret_cast<int4*>(dst.p[j] + (int64_t)drow * dst_stride + m * full_row +
-                                   (int64_t)a.rank * slice_bytes);
+                                   hb * head_bytes);
     }
     for (int v0 = 0; v0 < vpc; v0 += 32 * kUnroll) {
       int4 val[kUnroll];
@@ -114,11 +125,19 @@ int check_a2a(const FspA2A* a, const void* src, void* const* peer_dst) {
                 "degree must be a power of two in [1, 8] (got %d)", a->degree);
   FSP_CHECK_ARG(a->rank >= 0 && a->rank < a->degree, "rank %d outside group of %d", a->rank,
                 a->degree);
-  FSP_CHECK_ARG(a->n_heads % a->degree == 0, "n_heads (%d) not divisible by degree (%d)",
-                a->n_heads, a->degree);
-  FSP_CHECK_ARG(a->rows_per_rank >= 0 && a->n_mats >= 1 && a->head_dim >= 8, "bad sizes");
-  FSP_CHECK_ARG(((int64_t)(a->n_heads / a->degree) * a->head_dim * 2) % 16 == 0,
-                "head slice must be a multiple of 16 bytes");
+  FSP_CHECK_ARG(a->rows_per_rank >= 0 && a->n_mats >= 1 && a->head_dim >= 8 &&
+                    a->head_dim % 8 == 0,
+                "bad sizes");
+  if (a->head_begin[a->degree] == 0) {
+    FSP_CHECK_ARG(a->n_heads % a->degree == 0,
+                  "n_heads (%d) not divisible by degree (%d) and no head_begin split given",
+                  a->n_heads, a->degree);
+  } else {
+    FSP_CHECK_ARG(a->head_begin[0] == 0 && a->head_begin[a->degree] == a->n_heads,
+                  "head_begin must run from 0 to n_heads");
+    for (int j = 0; j < a->degree; ++j)
+      FSP_CHECK_ARG(a->head_begin[j + 1] > a->head_begin[j], "member %d owns no heads", j);
+  }
   FSP_CHECK_ARG(a->src_stride % 8 == 0 && a->dst_stride % 8 == 0, "strides must be multiples of 8");
   for (int j = 0; j < a->degree; ++j)
     FSP_CHECK_ARG(peer_dst[j] != nullptr && ((uintptr_t)peer_dst[j] & 15) == 0,
@@ -131,21 +150,27 @@ int launch_a2a(const FspA2A* a, const void* src, void* const* peer_dst, const in
                void* stream) {
   int rc = check_a2a(a, src, peer_dst);
   if (rc) return rc;
-  const int64_t full = (int64_t)a->n_heads * a->head_dim * a->n_mats;
-  const int64_t slice = full / a->degree;
+  FspA2A n = *a;  // normalised copy: the even split spelled out
+  if (n.head_begin[n.degree] == 0)
+    for (int j = 0; j <= n.degree; ++j) n.head_begin[j] = j * (n.n_heads / n.degree);
+  for (int j = n.degree + 1; j <= kMaxDegree; ++j) n.head_begin[j] = n.n_heads;
+  int hmax = 0;
+  for (int j = 0; j < n.degree; ++j) hmax = std::max(hmax, n.head_begin[j + 1] - n.head_begin[j]);
+  const int64_t full = (int64_t)n.n_heads * n.head_dim * n.n_mats;
+  const int64_t slice = (int64_t)hmax * n.head_dim * n.n_mats;
   if (kSeq2Head)
-    FSP_CHECK_ARG(a->src_stride >= full && a->dst_stride >= slice, "strides too small");
+    FSP_CHECK_ARG(n.src_stride >= full && n.dst_stride >= slice, "strides too small");
   else
-    FSP_CHECK_ARG(a->src_stride >= slice && a->dst_stride >= full, "strides too small");
+    FSP_CHECK_ARG(n.src_stride >= slice && n.dst_stride >= full, "strides too small");
   PeerPtrs pp{};
-  for (int j = 0; j < a->degree; ++j) pp.p[j] = reinterpret_cast<uint8_t*>(peer_dst[j]);
-  const int64_t chunks = (int64_t)a->rows_per_rank * a->n_mats * a->degree;
+  for (int j = 0; j < n.degree; ++j) pp.p[j] = reinterpret_cast<uint8_t*>(peer_dst[j]);
+  const int64_t chunks = (int64_t)n.rows_per_rank * n.n_mats * n.degree;
   FSP_CHECK_ARG(chunks < (1ll << 32), "exchange too large");
   if (chunks == 0) return FSP_OK;
   int64_t blocks = (chunks + kThreads / 32 - 1) / (kThreads / 32);
   if (blocks > 148 * 8) blocks = 148 * 8;
   a2a_kernel<kSeq2Head><<<(unsigned)blocks, kThreads, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const uint8_t*>(src), pp, index, *a);
+      reinterpret_cast<const uint8_t*>(src), pp, index, n);
   FSP_LAUNCH_CHECK();
   return FSP_OK;
 }

@@ -30,7 +30,7 @@ import torch
 
 from . import ops
 from .profiling import EventTimer
-from .layout import GroupLayout, LayoutError, MicroBatchLayout, build_plan_layouts
+from .layout import GroupLayout, LayoutError, MicroBatchLayout, build_plan_layouts, head_split
 
 _ALIGN = 4096
 _SIGNAL_BYTES = 4096
@@ -82,8 +82,17 @@ class RankMicroBatch:
     pack_index: torch.Tensor | None = None  # int32 [R]
     unpack_table: torch.Tensor | None = None  # int32 [d*R]
     sched: ops.AttnSchedule | None = None
-    fwd_flops: float = 0.0                  # 2 * D * (H/d) * sum s^2 (causal, FA convention)
+    fwd_flops: float = 0.0                  # 2 * D * H_j * sum s^2 (causal, FA convention)
     in_place: bool = False                  # d = 1: attention runs on the loader-order rows
+    head_begin: list[int] = field(default_factory=list)  # group's head split [d+1]
+
+    @property
+    def n_heads_local(self) -> int:        # H_j: heads this rank attends over
+        return self.head_begin[self.j + 1] - self.head_begin[self.j]
+
+    @property
+    def heads_stride(self) -> int:         # max_j H_j: head slots per matrix when sharded
+        return max(b - a for a, b in zip(self.head_begin, self.head_begin[1:]))
 
 
 @dataclass
@@ -132,7 +141,8 @@ class FlexSPExecutor:
                 mbs.append(RankMicroBatch(lay, None, -1, 0, np.zeros(0, dtype=np.int64)))
             else:
                 local = grp.local_tokens(j)
-                rmb = RankMicroBatch(lay, grp, j, int(local.shape[0]), local)
+                rmb = RankMicroBatch(lay, grp, j, int(local.shape[0]), local,
+                                     head_begin=head_split(self.n_heads, grp.degree))
                 rmb.pack_index = torch.from_numpy(grp.pack_index(j)).to(self.device)
                 rmb.unpack_table = torch.from_numpy(
                     np.ascontiguousarray(grp.unpack_table().reshape(-1))).to(self.device)
@@ -149,15 +159,16 @@ class FlexSPExecutor:
                     rmb.in_place = True
                 else:
                     rmb.sched = ops.AttnSchedule.build(grp.cu_seqlens, self.device,
-                                                       self.n_heads // grp.degree,
+                                                       rmb.n_heads_local,
                                                        total_rows=grp.padded_tokens,
                                                        head_dim=self.head_dim)
                 seg = np.diff(grp.cu_seqlens).astype(np.float64)
-                rmb.fwd_flops = 2.0 * self.head_dim * (self.n_heads // grp.degree) * float((seg ** 2).sum())
+                rmb.fwd_flops = 2.0 * self.head_dim * rmb.n_heads_local * float((seg ** 2).sum())
                 mbs.append(rmb)
             # heap regions must be identical on every rank: size by the max over ranks
             for g in lay.groups:
-                max_recv = max(max_recv, g.padded_tokens * (hd // g.degree))
+                max_recv = max(max_recv, g.padded_tokens * -(-self.n_heads // g.degree) *
+                               self.head_dim)
                 for jj in range(g.degree):
                     max_local = max(max_local, int((g.shard(jj) >= 0).sum()))
         off = {}
@@ -223,7 +234,7 @@ class FlexSPExecutor:
             return None, None
         H, D = self.n_heads, self.head_dim
         d, j, R = grp.degree, mb.j, grp.rows_per_rank
-        hs = H // d
+        hn, hm, hb = mb.n_heads_local, mb.heads_stride, mb.head_begin
         ranks = grp.ranks
         if qkv_local.shape[0] != mb.n_local:
             raise ValueError(f"rank {self.rank} expects {mb.n_local} local rows, got {qkv_local.shape[0]}")
@@ -236,33 +247,36 @@ class FlexSPExecutor:
                                       self.scale, out=out_local)
             return out_local, (qkv_local, out_local, lse)
         off = sp.offsets
-        recv = self.heap.view(off["qkv_recv"], (grp.padded_tokens, 3, hs, D), torch.bfloat16)
-        sent = float((d - 1) * R * hs * D * 2)  # NVLink bytes this rank sends per matrix
-        with self.timer.span("a2a", 3 * sent):
-            self._a2a_qkv(sp, mb, qkv_local, grp, R, hs)
+        T = grp.padded_tokens
+        recv = self.heap.view(off["qkv_recv"], (T, 3, hm, D), torch.bfloat16)
+        # NVLink bytes per matrix: seq2head sends the peers' head slices of R rows,
+        # head2seq sends this rank's head slice of (d-1)*R rows
+        sent_in = float(R * (H - hn) * D * 2)
+        sent_out = float((d - 1) * R * hn * D * 2)
+        with self.timer.span("a2a", 3 * sent_in):
+            self._a2a_qkv(sp, mb, qkv_local, grp, R, hm)
             self._barrier(ranks, self._next_epoch())
-        o_heads = self._workspace("o_heads", grp.padded_tokens * hs * D, torch.bfloat16).view(
-            grp.padded_tokens, hs, D)
+        o_heads = self._workspace("o_heads", T * hm * D, torch.bfloat16).view(T, hm, D)
         with self.timer.span("attn_fwd", mb.fwd_flops):
-            o_heads, lse = ops.attn_fwd(recv[:, 0], recv[:, 1], recv[:, 2], mb.sched, self.scale,
-                                        out=o_heads)
+            _, lse = ops.attn_fwd(recv[:, 0, :hn], recv[:, 1, :hn], recv[:, 2, :hn], mb.sched,
+                                  self.scale, out=o_heads[:, :hn])
         out_local, _ = self.local_buffers(sp, mb)
-        with self.timer.span("a2a", sent):
-            ops.a2a("head2seq", o_heads.view(grp.padded_tokens, hs * D),
+        with self.timer.span("a2a", sent_out):
+            ops.a2a("head2seq", o_heads.view(T, hm * D),
                     [self.heap.peer(r, off["out_local"]) for r in ranks], degree=d, rank=j,
                     rows_per_rank=R, n_mats=1, n_heads=H, head_dim=D, dst_stride=H * D,
-                    index=mb.unpack_table)
+                    index=mb.unpack_table, head_begin=hb)
             self._barrier(ranks, self._next_epoch())
-        return out_local, (recv, o_heads, lse)
+        return out_local, (recv[:, :, :hn], o_heads[:, :hn], lse)
 
-    def _a2a_qkv(self, sp, mb, qkv_local, grp, R, hs):
+    def _a2a_qkv(self, sp, mb, qkv_local, grp, R, hm):
         H, D, d, j = self.n_heads, self.head_dim, grp.degree, mb.j
         off = sp.offsets
         ops.a2a("seq2head", qkv_local.view(mb.n_local, -1) if mb.n_local else
                 qkv_local.reshape(0, 3 * H * D),
                 [self.heap.peer(r, off["qkv_recv"]) for r in grp.ranks], degree=d, rank=j,
-                rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * hs * D,
-                index=mb.pack_index)
+                rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * hm * D,
+                index=mb.pack_index, head_begin=mb.head_begin)
 
     def micro_batch_backward(self, sp: StepPlan, mb: RankMicroBatch, saved, dout_local: torch.Tensor):
         """Backward of micro_batch_forward: dout_local [n_local, H, D] -> dqkv_local view."""
@@ -286,31 +300,32 @@ class FlexSPExecutor:
                              dv=dqkv_local[:, 2], dq_accum=dq_acc, delta=delta)
             return dqkv_local
         d, j, R = grp.degree, mb.j, grp.rows_per_rank
-        hs = H // d
+        hn, hm, hb = mb.n_heads_local, mb.heads_stride, mb.head_begin
         ranks = grp.ranks
         off = sp.offsets
-        do_recv = self.heap.view(off["do_recv"], (grp.padded_tokens, hs, D), torch.bfloat16)
-        sent = float((d - 1) * R * hs * D * 2)
-        with self.timer.span("a2a", sent):
+        T = grp.padded_tokens
+        do_recv = self.heap.view(off["do_recv"], (T, hm, D), torch.bfloat16)
+        sent_in = float(R * (H - hn) * D * 2)
+        sent_out = float((d - 1) * R * hn * D * 2)
+        with self.timer.span("a2a", sent_in):
             ops.a2a("seq2head", dout_local.reshape(mb.n_local, H * D),
                     [self.heap.peer(r, off["do_recv"]) for r in ranks], degree=d, rank=j,
-                    rows_per_rank=R, n_mats=1, n_heads=H, head_dim=D, dst_stride=hs * D,
-                    index=mb.pack_index)
+                    rows_per_rank=R, n_mats=1, n_heads=H, head_dim=D, dst_stride=hm * D,
+                    index=mb.pack_index, head_begin=hb)
             self._barrier(ranks, self._next_epoch())
-        T = grp.padded_tokens
-        dqkv_heads = self._workspace("dqkv_heads", T * 3 * hs * D, torch.bfloat16).view(T, 3, hs, D)
-        dq_acc = self._workspace("dq_accum", T * hs * D, torch.float32)
-        delta = self._workspace("delta", hs * T, torch.float32)
+        dqkv_heads = self._workspace("dqkv_heads", T * 3 * hm * D, torch.bfloat16).view(T, 3, hm, D)
+        dq_acc = self._workspace("dq_accum", T * hn * D, torch.float32)
+        delta = self._workspace("delta", hn * T, torch.float32)
         with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
-            ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, do_recv, lse, mb.sched,
-                         self.scale, dq=dqkv_heads[:, 0], dk=dqkv_heads[:, 1],
-                         dv=dqkv_heads[:, 2], dq_accum=dq_acc, delta=delta)
+            ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, do_recv[:, :hn], lse,
+                         mb.sched, self.scale, dq=dqkv_heads[:, 0, :hn], dk=dqkv_heads[:, 1, :hn],
+                         dv=dqkv_heads[:, 2, :hn], dq_accum=dq_acc, delta=delta)
         _, dqkv_local = self.local_buffers(sp, mb)
-        with self.timer.span("a2a", 3 * sent):
-            ops.a2a("head2seq", dqkv_heads.view(T, 3 * hs * D),
+        with self.timer.span("a2a", 3 * sent_out):
+            ops.a2a("head2seq", dqkv_heads.view(T, 3 * hm * D),
                     [self.heap.peer(r, off["dqkv_local"]) for r in ranks], degree=d, rank=j,
                     rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * H * D,
-                    index=mb.unpack_table)
+                    index=mb.unpack_table, head_begin=hb)
             self._barrier(ranks, self._next_epoch())
         return dqkv_local
 

@@ -99,6 +99,20 @@ class MicroBatchLayout:
         return sum(g.total_tokens for g in self.groups)
 
 
+def head_split(n_heads: int, degree: int) -> list[int]:
+    """Heads of the `degree` members of a group: member j owns [b[j], b[j+1]).  The first
+    n_heads % degree members take one extra head, so heads need not divide by the degree
+    (52 heads at d=8 -> 7,7,7,7,6,6,6,6; the reference leaves head divisibility open,
+    SPEC.md:352, and the 30B shape has 52 heads)."""
+    if degree < 1 or n_heads < degree:
+        raise LayoutError(f"{n_heads} heads cannot be split over SP degree {degree}")
+    base, extra = divmod(n_heads, degree)
+    b = [0]
+    for j in range(degree):
+        b.append(b[-1] + base + (1 if j < extra else 0))
+    return b
+
+
 def token_offsets(lengths: Sequence[int]) -> np.ndarray:
     """Loader-order start offset of every sequence of the batch (int64 [K+1])."""
     out = np.zeros(len(lengths) + 1, dtype=np.int64)
@@ -125,8 +139,8 @@ def build_microbatch_layout(micro_batch: Any, lengths: Sequence[int], world_size
         if prev_degree is not None and d > prev_degree:
             raise LayoutError("selected_groups must be in slot order (degree descending)")
         prev_degree = d
-        if n_heads is not None and n_heads % d:
-            raise LayoutError(f"{n_heads} heads not divisible by SP degree {d} (SPEC.md:352)")
+        if n_heads is not None and n_heads < d:
+            raise LayoutError(f"{n_heads} heads cannot be split over SP degree {d}")
         if r0 + d > world_size:
             raise LayoutError(f"groups need more than {world_size} ranks")
         idx = tuple(int(k) for k in _get(g, "sequence_indices"))

@@ -198,12 +198,14 @@ def _ptr_array(ptrs) -> ctypes.Array:
 
 def a2a(direction: str, src: torch.Tensor, peer_dst_ptrs, *, degree: int, rank: int,
         rows_per_rank: int, n_mats: int, n_heads: int, head_dim: int, dst_stride: int,
-        index: torch.Tensor | None = None) -> None:
+        index: torch.Tensor | None = None, head_begin=None) -> None:
     """One Ulysses exchange (Eq. 2 'seq2head' / Eq. 4 'head2seq') over peer pointers.
 
     `src` is a row-major CUDA tensor whose dim-0 stride is the source row stride;
     `peer_dst_ptrs[j]` is group member j's destination base (device address valid in
     this process); `dst_stride` is the destination row stride in elements.
+    `head_begin` ([degree+1] prefix offsets, layout.head_split) selects an uneven head
+    split; the head-sharded side then holds n_mats x max_j(H_j) x D per row.
     """
     _require_cuda(src)
     if index is not None:
@@ -212,6 +214,11 @@ def a2a(direction: str, src: torch.Tensor, peer_dst_ptrs, *, degree: int, rank: 
             raise ValueError("a2a index must be int32")
     a = capi.FspA2A(degree, rank, rows_per_rank, n_mats, n_heads, head_dim, src.stride(0),
                     dst_stride)
+    if head_begin is not None:
+        if len(head_begin) != degree + 1:
+            raise ValueError("head_begin needs degree + 1 entries")
+        for j, b in enumerate(head_begin):
+            a.head_begin[j] = int(b)
     fn = capi.load().fsp_a2a_seq2head if direction == "seq2head" else capi.load().fsp_a2a_head2seq
     if direction not in ("seq2head", "head2seq"):
         raise ValueError(direction)

@@ -11,6 +11,9 @@ Outputs (all small JSON/NPZ, committed):
   c2_n{N}_{flexsp,static}.json   C2 long-tail batch (gen_longtail(64, pareto 1.1, 32K),
                   SURVEY.md §8d) planned for N = 1, 2, 4, 8 B200 with the B200
                   attention-layer coefficients below — these are the bench's plans
+  c3_n{N}_*.json, c4_n{N}_*.json   C3 (13B-shape, H=40) / C4 (30B-shape, H=52) batches
+                  planned with the fitted B200 coefficients (`--scale-configs` regenerates
+                  only these)
   rand_*.json     random small instances (N = 4, 8) for layout parity
   attn_small.npz  attention golden vectors from oracle/attention_ref.py (fp32), checked
                   against torch SDPA when generated
@@ -143,5 +146,45 @@ def main():
         print(key, hashlib.sha256(text.encode()).hexdigest()[:16], round(t, 6))
 
 
+# ---- C3 / C4: 13B-shape (H=40) and 30B-shape (H=52) attention layers.
+# Coefficients: the B200-fitted C2 coefficients (profiles/r01_calibration.json, H=32,
+# scripts/calibrate.py) with the per-head terms scaled by H/32 — attention FLOPs, HBM bytes,
+# NVLink bytes and activation memory per token are all linear in H at fixed D=128.
+SCALE_CONFIGS = {
+    "c3": {"heads": 40, "gen": (32, ("pareto", 1.1, 1024), 131072)},
+    "c4": {"heads": 52, "gen": (64, ("pareto", 0.9, 1024), 393216)},
+}
+
+
+def scaled_coeffs(heads: int) -> CostCoefficients:
+    cal = json.loads((ROOT / "profiles" / "r01_calibration.json").read_text())["coefficients"]
+    f = heads / 32.0
+    return CostCoefficients(alpha1=cal["alpha1"] * f, alpha2=cal["alpha2"] * f, beta1=cal["beta1"],
+                            alpha3=cal["alpha3"] * f, beta2=cal["beta2"],
+                            m_token=cal["m_token"] * f, m_ms=cal["m_ms"])
+
+
+def make_scale_configs():
+    for name, spec in SCALE_CONFIGS.items():
+        k, dist_, mx = spec["gen"]
+        b = gen_longtail(k, dist_, mx, seed=0)[0]
+        co = scaled_coeffs(spec["heads"])
+        for n in (1, 2, 4, 8):
+            cl = b200_cluster(n)
+            extra = {"coefficients": co.to_json_dict(), "cluster": cl.to_json_dict(),
+                     "heads": spec["heads"]}
+            p = solve_batch(b, cl, co, SolveConfig(jobs=8, time_limit=60))
+            dump(f"{name}_n{n}_flexsp.json", plan_doc(p, b, extra))
+            s = plan_static(b, cl, co, n)
+            dump(f"{name}_n{n}_static.json", plan_doc(s, b, extra))
+            print(f"{name} N={n}: {len(b.lengths)} seqs, {sum(b.lengths)} tokens, max {max(b.lengths)}; "
+                  f"flexsp {p.predicted_total_time:.4f}s "
+                  f"{[sorted((g.degree for g in mb.selected_groups), reverse=True) for mb in p.micro_batches]}"
+                  f" static {s.predicted_total_time:.4f}s", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if "--scale-configs" in sys.argv:  # C3 / C4 plans only
+        make_scale_configs()
+    else:
+        main()

@@ -43,30 +43,33 @@ def test_pack_unpack_bit_exact():
         assert torch.equal(back.cpu(), ref2)
 
 
-@pytest.mark.parametrize("degree", [1, 2, 4, 8])
-def test_a2a_emulated_group_bit_exact(degree):
+@pytest.mark.parametrize("degree,H", [(1, 8), (2, 8), (4, 8), (8, 8), (2, 5), (4, 10), (8, 13)])
+def test_a2a_emulated_group_bit_exact(degree, H):
     """seq2head (fused pack) and head2seq (fused unpack) for every member of a group,
-    against the numpy restatement of Eqs. (2)/(4) on the oracle's layout tables."""
+    against the numpy restatement of Eqs. (2)/(4) on the oracle's layout tables; H not
+    divisible by the degree exercises the uneven head split."""
     ops = _ops()
-    from paper_2412_01523_b200.layout import build_microbatch_layout
-    H, D = 8, 64
+    from paper_2412_01523_b200.layout import build_microbatch_layout, head_split
+    D = 64
     lengths = [333, 1, 128, 77, 1000]
     mb = {"selected_groups": [{"slot_id": 0, "degree": degree, "sequence_indices": [2, 0, 4, 1, 3]}]}
     lay = build_microbatch_layout(mb, lengths, degree, n_heads=H)
     grp = lay.groups[0]
     T = sum(lengths)
-    g = torch.Generator().manual_seed(degree)
+    g = torch.Generator().manual_seed(degree * 100 + H)
     x = torch.randint(-30000, 30000, (T, 3, H, D), generator=g, dtype=torch.int16)  # loader order
-    R, hs = grp.rows_per_rank, H // degree
+    hb = head_split(H, degree)
+    R, hm = grp.rows_per_rank, max(b - a for a, b in zip(hb, hb[1:]))
     locals_ = [x[torch.from_numpy(grp.local_tokens(j))].contiguous().cuda() for j in range(degree)]
-    recv = [torch.full((grp.padded_tokens, 3, hs, D), 7, dtype=torch.int16, device="cuda")
+    recv = [torch.full((grp.padded_tokens, 3, hm, D), 7, dtype=torch.int16, device="cuda")
             for _ in range(degree)]
     for j in range(degree):
         idx = torch.from_numpy(grp.pack_index(j)).cuda()
         src = locals_[j].view(locals_[j].shape[0], -1) if locals_[j].shape[0] else \
             locals_[j].reshape(0, 3 * H * D)
         ops.a2a("seq2head", src, [r.data_ptr() for r in recv], degree=degree, rank=j,
-                rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * hs * D, index=idx)
+                rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * hm * D, index=idx,
+                head_begin=hb)
     torch.cuda.synchronize()
     perm = grp.perm
     xp = np.zeros((grp.padded_tokens, 3, H, D), dtype=np.int16)
@@ -74,14 +77,16 @@ def test_a2a_emulated_group_bit_exact(degree):
     shards = [xp[j * R:(j + 1) * R] for j in range(degree)]
     ref = layout_ref.ulysses_seq2head(shards, 3, H, D)
     for j in range(degree):
-        np.testing.assert_array_equal(recv[j].cpu().numpy(), ref[j])
+        got = recv[j].cpu().numpy()
+        np.testing.assert_array_equal(got[:, :, :hb[j + 1] - hb[j]], ref[j])
+        assert (got[:, :, hb[j + 1] - hb[j]:] == 7).all()  # padding head slots untouched
     # head2seq back into loader-order local buffers: exact round trip
     outs = [torch.zeros_like(l) for l in locals_]
     table = torch.from_numpy(np.ascontiguousarray(grp.unpack_table().reshape(-1))).cuda()
     for j in range(degree):
         ops.a2a("head2seq", recv[j].view(grp.padded_tokens, -1), [o.data_ptr() for o in outs],
                 degree=degree, rank=j, rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D,
-                dst_stride=3 * H * D, index=table)
+                dst_stride=3 * H * D, index=table, head_begin=hb)
     torch.cuda.synchronize()
     for j in range(degree):
         assert torch.equal(outs[j].cpu(), locals_[j].cpu())

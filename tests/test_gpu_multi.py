@@ -13,18 +13,20 @@ import torch
 
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
-CASES = [(2, "c1_flexsp_2tier.json"), (2, "c1_static2.json"), (4, "rand0_n4_flexsp.json"),
-         (4, "rand2_n4_flexsp.json"), (8, "rand1_n8_flexsp.json")]
+CASES = [(2, "c1_flexsp_2tier.json", 8), (2, "c1_static2.json", 8), (4, "rand0_n4_flexsp.json", 8),
+         (4, "rand2_n4_flexsp.json", 8), (8, "rand1_n8_flexsp.json", 8),
+         # uneven head splits: 5 heads over 2 ranks, 10 over 4
+         (2, "c1_static2.json", 5), (4, "rand0_n4_flexsp.json", 10)]
 
 
-@pytest.mark.parametrize("n,plan", CASES)
-def test_mgpu_step_matches_oracle(n, plan):
+@pytest.mark.parametrize("n,plan,heads", CASES)
+def test_mgpu_step_matches_oracle(n, plan, heads):
     if torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     env = dict(os.environ, OMP_NUM_THREADS="4")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + n),
-           str(ROOT / "scripts" / "mgpu_parity.py"), plan]
+           str(ROOT / "scripts" / "mgpu_parity.py"), plan, str(heads)]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
     assert '"ok": true' in res.stdout

@@ -103,8 +103,9 @@ def test_layout_errors():
     with pytest.raises(LayoutError):
         build_microbatch_layout(mb, [5], 2)
     mb = {"selected_groups": [{"slot_id": 0, "degree": 2, "sequence_indices": [0]}]}
-    with pytest.raises(LayoutError):  # 3 heads not divisible by degree 2
-        build_microbatch_layout(mb, [5], 2, n_heads=3)
+    with pytest.raises(LayoutError):  # 1 head cannot be split over 2 members
+        build_microbatch_layout(mb, [5], 2, n_heads=1)
+    build_microbatch_layout(mb, [5], 2, n_heads=3)  # uneven split 2 + 1 is allowed (H5)
     with pytest.raises(LayoutError):
         load_plan({"schema": 2})
 
@@ -119,3 +120,14 @@ def test_padding_and_tiny_groups():
     np.testing.assert_array_equal(g.cu_seqlens, [0, 3, 5])
     assert g.local_tokens(3).size == 0
     np.testing.assert_array_equal(g.pack_index(2), [0, -1])
+
+
+def test_head_split_matches_oracle():
+    from oracle import layout_ref
+    from paper_2412_01523_b200.layout import head_split
+    for h in (1, 4, 5, 13, 32, 40, 52):
+        for d in (1, 2, 4, 8):
+            if h >= d:
+                assert head_split(h, d) == layout_ref.head_split(h, d), (h, d)
+    with pytest.raises(LayoutError):
+        head_split(4, 8)

@@ -64,15 +64,17 @@ def _ulysses_worker(rank, world, port, q, cu, out_path):
     dist.destroy_process_group()
 
 
-def test_ulysses_gloo_world2_equals_single_process(tmp_path):
-    """Eq. (2)-(4) on two gloo ranks == attention without SP (SP is an identity)."""
+@pytest.mark.parametrize("heads", [4, 5])
+def test_ulysses_gloo_world2_equals_single_process(tmp_path, heads):
+    """Eq. (2)-(4) on two gloo ranks == attention without SP (SP is an identity); 5 heads
+    exercise the uneven head split (3 + 2)."""
     g = torch.Generator().manual_seed(11)
     lens = [97, 1, 200, 33]
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     T = int(cu[-1])
     Tp = -(-T // 2) * 2
-    qkv = torch.zeros(Tp, 3, 4, 16)
-    qkv[:T] = torch.randn(T, 3, 4, 16, generator=g)
+    qkv = torch.zeros(Tp, 3, heads, 16)
+    qkv[:T] = torch.randn(T, 3, heads, 16, generator=g)
     port = 29500 + os.getpid() % 1000
     mp.spawn(_ulysses_worker, args=(2, port, qkv, cu, str(tmp_path / "o")), nprocs=2)
     got = torch.cat([torch.load(tmp_path / f"o.{r}") for r in range(2)])[:T]
@@ -90,3 +92,23 @@ def test_numpy_exchange_restatement_roundtrip():
     back = layout_ref.ulysses_head2seq(heads, M, H, D)
     for a, b in zip(back, shards):
         np.testing.assert_array_equal(a, b)
+
+
+def test_head_split_uneven():
+    assert layout_ref.head_split(52, 8) == [0, 7, 14, 21, 28, 34, 40, 46, 52]
+    assert layout_ref.head_split(32, 4) == [0, 8, 16, 24, 32]
+    assert layout_ref.head_split(3, 1) == [0, 3]
+
+
+def test_numpy_exchange_restatement_roundtrip_uneven_heads():
+    rng = np.random.default_rng(1)
+    d, R, M, H, D = 8, 2, 3, 13, 2
+    shards = [rng.standard_normal((R, M, H, D)) for _ in range(d)]
+    heads = layout_ref.ulysses_seq2head(shards, M, H, D)
+    b = layout_ref.head_split(H, d)
+    for j in range(d):
+        assert heads[j].shape == (d * R, M, b[j + 1] - b[j], D)
+    np.testing.assert_array_equal(heads[5][3 * R:4 * R], shards[3][:, :, b[5]:b[6], :])
+    back = layout_ref.ulysses_head2seq(heads, M, H, D)
+    for a, c in zip(back, shards):
+        np.testing.assert_array_equal(a, c)
