@@ -399,14 +399,21 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
 // Warps: 0 TMA, 1 MMA, 2..9 compute (two per TMEM lane quadrant, 32 of the 64 columns
 // each), 10..13 dQ reduction (one per quadrant, all 64 columns).
 #ifndef FSP_BWD_ABLATE
-#define FSP_BWD_ABLATE 0  // profiling ablations: 1 = skip gradient math, 2 = skip dQ readout
+#define FSP_BWD_ABLATE 0  // profiling ablations (bits): 1 = skip gradient math, 2 = skip dQ
+                          // readout, 4 = skip dQ^T MMAs, 8 = skip dK MMAs, 16 = plain
+                          // stores instead of dQ reductions, 32 = no dQ stores at all,
+                          // 64 = no dQ^T TMEM readout
 #endif
 #ifndef FSP_BWD_COMPUTE_WARPS
 #define FSP_BWD_COMPUTE_WARPS 16
 #endif
 constexpr int kV2Compute = FSP_BWD_COMPUTE_WARPS;  // 8 or 16: 2 or 4 warps per lane quadrant
 constexpr int kV2Cols = 64 / (kV2Compute / 4);      // query columns per compute warp
-constexpr int kV2Reduce = 4;
+#ifndef FSP_BWD_REDUCE_WARPS
+#define FSP_BWD_REDUCE_WARPS 4
+#endif
+constexpr int kV2Reduce = FSP_BWD_REDUCE_WARPS;  // 4 or 8: 1 or 2 warps per lane quadrant
+constexpr int kV2RedCols = 64 / (kV2Reduce / 4);   // dQ^T columns (query rows) per warp
 constexpr int kV2Threads = 64 + 32 * (kV2Compute + kV2Reduce);
 constexpr uint32_t kV2ColS = 256, kV2ColDP = 384;
 
@@ -422,6 +429,22 @@ struct BwdSmemV2 {
   static constexpr int kBar = kStat + 4 * 128 * 4;
   static constexpr int kBytes = kBar + 256;
 };
+
+#ifndef FSP_BWD_TIMING
+#define FSP_BWD_TIMING 0  // profiling build: cycles the MMA issuer / compute warps spend waiting
+#endif
+#if FSP_BWD_TIMING
+__device__ unsigned long long g_bwd_wait[16];
+__device__ unsigned int g_bwd_done;
+#define FSP_TW(slot, call)                               \
+  do {                                                   \
+    const long long t0_ = clock64();                     \
+    call;                                                \
+    tw[slot] += clock64() - t0_;                         \
+  } while (0)
+#else
+#define FSP_TW(slot, call) call
+#endif
 
 __global__ void __launch_bounds__(kV2Threads, 1)
     attn_bwd_kernel_v2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -516,21 +539,26 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       const uint32_t v_base = smem_u32(smem + L::kV);
       const uint32_t ring_base = smem_u32(smem + L::kRing);
       const uint32_t ds_base = smem_u32(smem + L::kDS);
-      mbar_wait(bar_kv, 0);
+#if FSP_BWD_TIMING
+      long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const long long t_start = clock64();
+#endif
+      FSP_TW(6, mbar_wait(bar_kv, 0));
       auto grads = [&](int u) {
         const int it = u >> 1, h = u & 1;
         const int sq = (2 * u) % L::kSlots, sd = (2 * u + 1) % L::kSlots;
         const uint32_t q_base = ring_base + sq * L::kHalfBytes;
         const uint32_t do_base = ring_base + sd * L::kHalfBytes;
         const uint32_t dsb = ds_base + h * 16384;
-        mbar_wait(p_ready + h, it & 1);
+        FSP_TW(3, mbar_wait(p_ready + h, it & 1));
         tc_fence_after();
         // dQ^T first and committed on its own, so the reduction warps drain it while dV and
         // dK (and the next S^T) keep the tensor core busy: dP^T(u+2) waits on that drain.
-        if (u >= 2) mbar_wait(tm_free + h, ((u >> 1) - 1) & 1);  // dQ^T(u-2) drained
+        if (u >= 2) FSP_TW(4, mbar_wait(tm_free + h, ((u >> 1) - 1) & 1));  // dQ^T(u-2) drained
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 kv rows)
+          if (!(FSP_BWD_ABLATE & 4))
           mma_ss(tmem + kV2ColDP + h * 64, make_sdesc_sw128(k_base + kk * 2048, 16384, 1024),
                  make_sdesc_sw128(dsb + kk * 2048, 16384, 1024), idesc_dqt, kk > 0);
         tc_commit(dq_full + h);
@@ -545,6 +573,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                  (u > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q_h
+          if (!(FSP_BWD_ABLATE & 8))
           mma_ss(tmem + kColDK, make_sdesc_sw128(dsb + kk * 32, 16, 1024),
                  make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
                  (u > 0 || kk > 0) ? 1u : 0u);
@@ -559,7 +588,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         const uint32_t do_base = ring_base + sd * L::kHalfBytes;
         // S^T(u) overwrites P^T(u-2), read by dV of grads(u-2) (issued earlier, in order);
         // dP^T(u) overwrites dQ^T(u-2): wait until the reduction warps drained it.
-        mbar_wait(ring_full + sq, ((2 * u) / L::kSlots) & 1);
+        FSP_TW(0, mbar_wait(ring_full + sq, ((2 * u) / L::kSlots) & 1));
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -568,8 +597,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                  make_sdesc_sw128(q_base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_s,
                  kk > 0);
         }
-        if (u >= 2) mbar_wait(tm_free + h, ((u >> 1) - 1) & 1);
-        mbar_wait(ring_full + sd, ((2 * u + 1) / L::kSlots) & 1);
+        if (u >= 2) FSP_TW(1, mbar_wait(tm_free + h, ((u >> 1) - 1) & 1));
+        FSP_TW(2, mbar_wait(ring_full + sd, ((2 * u + 1) / L::kSlots) & 1));
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -582,6 +611,23 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         if (u >= 1) grads(u - 1);
       }
       if (n_u > 0) grads(n_u - 1);
+#if FSP_BWD_TIMING
+      tw[7] = clock64() - t_start;
+      for (int i = 0; i < 8; ++i) atomicAdd(&g_bwd_wait[i], (unsigned long long)tw[i]);
+      atomicAdd(&g_bwd_wait[8], (unsigned long long)n_u);
+      __threadfence();
+      if (atomicAdd(&g_bwd_done, 1u) == gridDim.x - 1) {
+        printf("bwd MMA issuer cycles (sum over CTAs): units %llu total %llu | ring_full(Q) %llu "
+               "tm_free(dP) %llu ring_full(dO) %llu p_ready %llu tm_free(dQ) %llu kv %llu\n",
+               g_bwd_wait[8], g_bwd_wait[7], g_bwd_wait[0], g_bwd_wait[1], g_bwd_wait[2],
+               g_bwd_wait[3], g_bwd_wait[4], g_bwd_wait[6]);
+        printf("bwd compute warp0 cycles: s_full wait %llu busy %llu | reduce warp0: dq_full "
+               "wait %llu busy %llu\n", g_bwd_wait[9], g_bwd_wait[10], g_bwd_wait[11],
+               g_bwd_wait[12]);
+        for (int i = 0; i < 16; ++i) g_bwd_wait[i] = 0;
+        g_bwd_done = 0;
+      }
+#endif
     }
     __syncwarp();
   } else if (warp < 2 + kV2Compute) {
@@ -609,7 +655,13 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       const int c0 = h * 64 + ch * kV2Cols;  // query column offset inside the 128-row tile
       const float* ls = lse_s + buf * 128 + c0;
       const float* dl = delta_s + buf * 128 + c0;
+#if FSP_BWD_TIMING
+      const long long tq0 = clock64();
+#endif
       mbar_wait(s_full + h, it & 1);
+#if FSP_BWD_TIMING
+      if (cw == 0 && lane == 0) atomicAdd(&g_bwd_wait[9], (unsigned long long)(clock64() - tq0));
+#endif
       tc_fence_after();
       if (FSP_BWD_ABLATE & 1) {  // profiling ablation: no gradient math
         tc_fence_before();
@@ -665,6 +717,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready + h);
+#if FSP_BWD_TIMING
+      if (cw == 0 && lane == 0) atomicAdd(&g_bwd_wait[10], (unsigned long long)(clock64() - tq0));
+#endif
     };
     const bool stat_thread = ctid < 256;
     float stat = (n_it > 0 && stat_thread) ? load_stat(0) : 0.f;
@@ -719,12 +774,20 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     // [H, T, D] fp32 so a warp's 32 lanes add 128 contiguous bytes per query row and the
     // row stride (D*4 = 512 B) folds into the instruction's immediate offset.
     const uint32_t quad = warp & 3;
+    const int part = (int)(warp - 2 - kV2Compute) >> 2;  // which kV2RedCols of the 64 columns
     const int r = quad * 32 + lane;
     const uint32_t lane_addr = (quad * 32u) << 16;
     float* head_base = p.dq_accum + ((int64_t)head * p.total_rows + seq_start) * D + r;
     for (int u = 0; u < n_u; ++u) {
       const int it = u >> 1, h = u & 1;
+#if FSP_BWD_TIMING
+      const long long tr0 = clock64();
+#endif
       mbar_wait(dq_full + h, it & 1);
+#if FSP_BWD_TIMING
+      const long long tr1 = clock64();
+      if (warp == 2 + kV2Compute && lane == 0) atomicAdd(&g_bwd_wait[11], (unsigned long long)(tr1 - tr0));
+#endif
       tc_fence_after();
       if (FSP_BWD_ABLATE & 2) {  // profiling ablation: no dQ readout / reductions
         tc_fence_before();
@@ -732,30 +795,47 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         if (lane == 0) mbar_arrive(tm_free + h);
         continue;
       }
-      uint32_t qr[64];
-      tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64, *reinterpret_cast<uint32_t(*)[32]>(qr));
-      tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + 32,
-                *reinterpret_cast<uint32_t(*)[32]>(qr + 32));
-      tmem_ld_wait();
+      uint32_t qr[kV2RedCols];
+      if (FSP_BWD_ABLATE & 64) {  // profiling ablation: no TMEM readout (reduce zeros)
+#pragma unroll
+        for (int i = 0; i < kV2RedCols; ++i) qr[i] = 0u;
+      } else {
+        tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + part * kV2RedCols,
+                  *reinterpret_cast<uint32_t(*)[32]>(qr));
+        if (kV2RedCols == 64)
+          tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + 32,
+                    *reinterpret_cast<uint32_t(*)[32]>(qr + (kV2RedCols == 64 ? 32 : 0)));
+        tmem_ld_wait();
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tm_free + h);
-      const int qb = (kt + it) * kTile + h * 64;  // first query row of this half (in sequence)
+      // first query row of this warp's columns (in sequence)
+      const int qb = (kt + it) * kTile + h * 64 + part * kV2RedCols;
       float* base = head_base + (int64_t)qb * D;
       const int nvalid = seqlen - qb;
-      if (nvalid >= 64) {
+      if (FSP_BWD_ABLATE & 32) {  // profiling ablation: read dQ^T out of TMEM, drop it
+        if (nvalid == -12345) base[0] = __uint_as_float(qr[0] + qr[kV2RedCols - 1]);
+      } else if (FSP_BWD_ABLATE & 16) {  // profiling ablation: plain stores, no reductions
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
+        for (int i = 0; i < kV2RedCols; ++i)
+          if (i < nvalid) base[i * D] = __uint_as_float(qr[i]);
+      } else if (nvalid >= kV2RedCols) {
+#pragma unroll
+        for (int i = 0; i < kV2RedCols; ++i)
           asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + i * D), "f"(__uint_as_float(qr[i]))
                        : "memory");
       } else {
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
+        for (int i = 0; i < kV2RedCols; ++i)
           if (i < nvalid)
             asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + i * D),
                          "f"(__uint_as_float(qr[i]))
                          : "memory");
       }
+#if FSP_BWD_TIMING
+      if (warp == 2 + kV2Compute && lane == 0) atomicAdd(&g_bwd_wait[12], (unsigned long long)(clock64() - tr1));
+#endif
     }
   }
   tc_fence_before();

@@ -44,6 +44,25 @@ except Exception as ex:
     print("bwd:", ex)
 if os.environ.get("NOFA"):
     raise SystemExit(0)
+if WL != "c2" and os.environ.get("CUDNN", "1") == "1":
+    # cuDNN's fused attention through torch SDPA (fixed-length batch, same causal FLOPs)
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        B, S = len(L), int(L[0])
+        qb = q.reshape(B, S, H, D).transpose(1, 2).contiguous()
+        kb = k.reshape(B, S, H, D).transpose(1, 2).contiguous()
+        vb = v.reshape(B, S, H, D).transpose(1, 2).contiguous()
+        dob = do.reshape(B, S, H, D).transpose(1, 2).contiguous()
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+            f = lambda: torch.nn.functional.scaled_dot_product_attention(qb, kb, vb, is_causal=True)
+            ms = timeit(f)
+            print(f"cudnn fwd: {ms:.3f} ms  {fl_fwd/ms/1e9:.1f} TFLOP/s")
+            qb.requires_grad_(); kb.requires_grad_(); vb.requires_grad_()
+            out = torch.nn.functional.scaled_dot_product_attention(qb, kb, vb, is_causal=True)
+            ms = timeit(lambda: torch.autograd.grad(out, (qb, kb, vb), dob, retain_graph=True))
+            print(f"cudnn bwd: {ms:.3f} ms  {2.5*fl_fwd/ms/1e9:.1f} TFLOP/s")
+    except Exception as ex:
+        print("cudnn:", repr(ex)[:300])
 try:
     from flash_attn import flash_attn_varlen_func
     cu_t = torch.from_numpy(cu).to(dev)
