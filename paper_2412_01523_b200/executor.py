@@ -167,8 +167,9 @@ class FlexSPExecutor:
                 mbs.append(rmb)
             # heap regions must be identical on every rank: size by the max over ranks
             for g in lay.groups:
-                max_recv = max(max_recv, g.padded_tokens * -(-self.n_heads // g.degree) *
-                               self.head_dim)
+                if g.degree > 1:  # d = 1 groups compute in place: no receive buffers
+                    max_recv = max(max_recv, g.padded_tokens * -(-self.n_heads // g.degree) *
+                                   self.head_dim)
                 for jj in range(g.degree):
                     max_local = max(max_local, int((g.shard(jj) >= 0).sum()))
         off = {}
