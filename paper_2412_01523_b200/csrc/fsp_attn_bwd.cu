@@ -404,6 +404,9 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
                           // stores instead of dQ reductions, 32 = no dQ stores at all,
                           // 64 = no dQ^T TMEM readout
 #endif
+#ifndef FSP_BWD_DS_TMEM
+#define FSP_BWD_DS_TMEM 1  // dS^T also goes to TMEM so dK += dS^T Q is a TS MMA
+#endif
 #ifndef FSP_BWD_COMPUTE_WARPS
 #define FSP_BWD_COMPUTE_WARPS 16
 #endif
@@ -572,11 +575,19 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                  make_sdesc_sw128(do_base + kk * 2048, 8192, 1024), idesc_dvdk,
                  (u > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q_h
-          if (!(FSP_BWD_ABLATE & 8))
-          mma_ss(tmem + kColDK, make_sdesc_sw128(dsb + kk * 32, 16, 1024),
-                 make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
-                 (u > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk) {  // dK += dS^T Q_h
+          if (FSP_BWD_ABLATE & 8) continue;
+          if (FSP_BWD_DS_TMEM)  // TS: dS^T from the second half of the writer warp's S columns
+            mma_ts(tmem + kColDK,
+                   tmem + kV2ColS + h * 64 + (16 * kk / kV2Cols) * kV2Cols + (16 * kk % kV2Cols) / 2 +
+                       kV2Cols / 2,
+                   make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
+                   (u > 0 || kk > 0) ? 1u : 0u);
+          else
+            mma_ss(tmem + kColDK, make_sdesc_sw128(dsb + kk * 32, 16, 1024),
+                   make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
+                   (u > 0 || kk > 0) ? 1u : 0u);
+        }
         tc_commit(ring_empty + sq);
         tc_commit(ring_empty + sd);
         if (u == n_u - 1) tc_commit(acc_done);
@@ -700,10 +711,18 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         pk[i / 2] = pack_bf16(p0, p1);
         dk[i / 2] = pack_bf16(d0, d1);
       }
-      if (kV2Cols == 32)  // own S columns
+      // own S columns: P^T (bf16 pairs) in the first half, dS^T in the second (FSP_BWD_DS_TMEM)
+      if (kV2Cols == 32) {
         tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, *reinterpret_cast<const uint32_t(*)[16]>(pk));
-      else
+        if (FSP_BWD_DS_TMEM)
+          tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 32 + 16,
+                    *reinterpret_cast<const uint32_t(*)[16]>(dk));
+      } else {
         tmem_st8(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, *reinterpret_cast<const uint32_t(*)[8]>(pk));
+        if (FSP_BWD_DS_TMEM)
+          tmem_st8(tmem + lane_addr + kV2ColS + h * 64 + ch * 16 + 8,
+                   *reinterpret_cast<const uint32_t(*)[8]>(dk));
+      }
       // dS^T row r, query columns [ch*kV2Cols, +kV2Cols) of this half: 16-byte chunks
       uint8_t* row = smem + L::kDS + h * 16384 + r * 128;
 #pragma unroll
