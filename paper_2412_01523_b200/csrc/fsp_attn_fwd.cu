@@ -297,6 +297,12 @@ constexpr int kF2Threads = 64 + 256;
 #define FSP_ABLATE_EXP 0
 #endif
 // one exponential pair in FSP_POLY_EVERY runs as a polynomial on the FMA pipe (0 = none)
+#ifndef FSP_FWD_PREFETCH
+#define FSP_FWD_PREFETCH 1  // 1: TMEM load of the next 32-column chunk overlaps this chunk's math
+#endif
+#ifndef FSP_FWD_ONEPASS
+#define FSP_FWD_ONEPASS 0  // 1: S row kept in registers between the max and exp passes
+#endif
 #ifndef FSP_POLY_EVERY
 #define FSP_POLY_EVERY 4
 #endif
@@ -324,6 +330,22 @@ __device__ __forceinline__ float ex2_poly(float x) {
   pf = fmaf(pf, f, 0.99992828f);
   return __int_as_float(__float_as_int(pf) + (__float_as_int(y) << 23));
 }
+
+#ifndef FSP_FWD_TIMING
+#define FSP_FWD_TIMING 0  // profiling build: cycles the MMA issuer / softmax warps spend waiting
+#endif
+#if FSP_FWD_TIMING
+__device__ unsigned long long g_fwd_wait[16];
+__device__ unsigned int g_fwd_done;
+#define FSP_FTW(slot, call)                              \
+  do {                                                   \
+    const long long t0_ = clock64();                     \
+    call;                                                \
+    tw[slot] += clock64() - t0_;                         \
+  } while (0)
+#else
+#define FSP_FTW(slot, call) call
+#endif
 
 __global__ void __launch_bounds__(kF2Threads, 1)
     attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q,
@@ -421,7 +443,11 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       const uint32_t qa = smem_u32(smem + L::kQA), qb = smem_u32(smem + L::kQB);
       const uint32_t k_base = smem_u32(smem + L::kK);
       const uint32_t v_base = smem_u32(smem + L::kV);
-      mbar_wait(bar_q, 0);
+#if FSP_FWD_TIMING
+      long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const long long t_start = clock64();
+#endif
+      FSP_FTW(5, mbar_wait(bar_q, 0));
       auto qk = [&](int x, int j) {  // S_x = Q_x K_j^T
         const uint32_t qbase = x ? qb : qa;
         const uint32_t kb = k_base + (j % L::kKStages) * L::kTileBytes;
@@ -437,7 +463,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         const uint32_t vb = v_base + (j & 1) * L::kTileBytes;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          mbar_wait(p_half + 2 * x + hh, j & 1);
+          FSP_FTW(x, mbar_wait(p_half + 2 * x + hh, j & 1));
           tc_fence_after();
 #pragma unroll
           for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
@@ -447,7 +473,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         }
       };
       auto wait_k = [&](int j) {
-        mbar_wait(k_full + j % L::kKStages, (j / L::kKStages) & 1);
+        FSP_FTW(2, mbar_wait(k_full + j % L::kKStages, (j / L::kKStages) & 1));
         tc_fence_after();
       };
       wait_k(0);
@@ -457,7 +483,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
         const bool next = j + 1 < n_kv;
-        mbar_wait(v_full + st, (j >> 1) & 1);
+        FSP_FTW(3, mbar_wait(v_full + st, (j >> 1) & 1));
         if (j < n_a) {
           pv(0, j);
           if (j + 1 < n_a) {
@@ -479,6 +505,21 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         tc_commit(v_empty + st);
         if (next) tc_commit(k_empty + (j + 1) % L::kKStages);
       }
+#if FSP_FWD_TIMING
+      tw[7] = clock64() - t_start;
+      for (int i = 0; i < 8; ++i) atomicAdd(&g_fwd_wait[i], (unsigned long long)tw[i]);
+      atomicAdd(&g_fwd_wait[8], (unsigned long long)(n_a + n_b));
+      __threadfence();
+      if (atomicAdd(&g_fwd_done, 1u) == gridDim.x - 1) {
+        printf("fwd MMA issuer cycles (sum over CTAs): tile-steps %llu total %llu | p_half A %llu "
+               "p_half B %llu k_full %llu v_full %llu q %llu\n", g_fwd_wait[8], g_fwd_wait[7],
+               g_fwd_wait[0], g_fwd_wait[1], g_fwd_wait[2], g_fwd_wait[3], g_fwd_wait[5]);
+        printf("fwd softmax warp (tile A, quad 0): s_full wait %llu busy %llu\n", g_fwd_wait[9],
+               g_fwd_wait[10]);
+        for (int i = 0; i < 16; ++i) g_fwd_wait[i] = 0;
+        g_fwd_done = 0;
+      }
+#endif
     }
     __syncwarp();
   } else {
@@ -494,7 +535,14 @@ __global__ void __launch_bounds__(kF2Threads, 1)
     float m = -INFINITY;  // exponent base (scaled, log2 units)
     float l = 0.f;
     for (int j = 0; j < n_x; ++j) {
+#if FSP_FWD_TIMING
+      const long long ts0 = clock64();
+#endif
       mbar_wait(s_full + x, j & 1);
+#if FSP_FWD_TIMING
+      const long long ts1 = clock64();
+      if (warp == 2 && lane == 0) atomicAdd(&g_fwd_wait[9], (unsigned long long)(ts1 - ts0));
+#endif
       tc_fence_after();
       if (FSP_ABLATE_EXP >= 2) {  // profiling ablations: 2 = no softmax work,
         // 3 = two passes of TMEM loads + P store, 4 = one pass of loads + P store
@@ -532,13 +580,33 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       const int lim = q_pos - j * 128;  // causal: column c valid iff c <= lim (diagonal tile)
       auto tile_body = [&](auto diag_c) {
         constexpr bool kDiag = decltype(diag_c)::value;
-        // pass 1: row max; four independent FMNMX3 chains, chunked TMEM loads
+        // pass 1: row max; four independent FMNMX3 chains.  FSP_FWD_ONEPASS keeps the whole
+        // 128-column row in registers (one TMEM round trip per tile), otherwise chunked
+        // loads are repeated in pass 2.
         float mxs[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#if FSP_FWD_ONEPASS
+        uint32_t row_s[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_addr + s_col + 32 * c, row_s[c]);
+        tmem_ld_wait();
+#endif
+#if FSP_FWD_PREFETCH && !FSP_FWD_ONEPASS
+        uint32_t buf[2][32];  // chunk c+1 is in flight while chunk c is processed
+        tmem_ld32(tmem + lane_addr + s_col, buf[0]);
+        tmem_ld_wait_tied(buf[0]);
+#endif
 #pragma unroll
         for (int c = 0; c < 128; c += 32) {
+#if FSP_FWD_ONEPASS
+          const uint32_t(&r)[32] = row_s[c / 32];
+#elif FSP_FWD_PREFETCH
+          uint32_t(&r)[32] = buf[(c / 32) & 1];
+          if (c + 32 < 128) tmem_ld32(tmem + lane_addr + s_col + c + 32, buf[((c / 32) + 1) & 1]);
+#else
           uint32_t r[32];
           tmem_ld32(tmem + lane_addr + s_col + c, r);
           tmem_ld_wait();
+#endif
 #pragma unroll
           for (int i = 0; i < 32; i += 8)
 #pragma unroll
@@ -550,6 +618,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
               }
               mxs[a] = fmax3(mxs[a], v0, v1);
             }
+#if FSP_FWD_PREFETCH && !FSP_FWD_ONEPASS
+          if (c + 32 < 128) tmem_ld_wait_tied(buf[((c / 32) + 1) & 1]);
+#endif
         }
         const float mx = fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3]));
         const float m_new = fmaxf(m, mx * sl2);
@@ -576,11 +647,23 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         // Packed fp32x2 math; one pair in four exponentiates on the FMA pipe (ex2_poly2).
         const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(-m, -m);
         uint64_t sum2[4] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
+#if FSP_FWD_PREFETCH && !FSP_FWD_ONEPASS
+        tmem_ld32(tmem + lane_addr + s_col, buf[0]);
+        tmem_ld_wait_tied(buf[0]);
+#endif
 #pragma unroll
         for (int c = 0; c < 128; c += 32) {
-          uint32_t r[32], pk[16];
+          uint32_t pk[16];
+#if FSP_FWD_ONEPASS
+          const uint32_t(&r)[32] = row_s[c / 32];
+#elif FSP_FWD_PREFETCH
+          uint32_t(&r)[32] = buf[(c / 32) & 1];
+          if (c + 32 < 128) tmem_ld32(tmem + lane_addr + s_col + c + 32, buf[((c / 32) + 1) & 1]);
+#else
+          uint32_t r[32];
           tmem_ld32(tmem + lane_addr + s_col + c, r);
           tmem_ld_wait();
+#endif
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             const uint64_t x2 =
@@ -611,6 +694,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(p_half + 2 * x);
           }
+#if FSP_FWD_PREFETCH && !FSP_FWD_ONEPASS
+          if (c + 32 < 128) tmem_ld_wait_tied(buf[((c / 32) + 1) & 1]);
+#endif
         }
         float sum_lo, sum_hi;
         f2_split(fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3])), sum_lo, sum_hi);
@@ -624,6 +710,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_half + 2 * x + 1);
+#if FSP_FWD_TIMING
+      if (warp == 2 && lane == 0) atomicAdd(&g_fwd_wait[10], (unsigned long long)(clock64() - ts1));
+#endif
     }
     // ------------------------------------------------------------ epilogue
     if (n_x > 0) {
