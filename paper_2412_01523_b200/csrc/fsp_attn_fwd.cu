@@ -300,9 +300,6 @@ constexpr int kF2Threads = 64 + 256;
 #ifndef FSP_FWD_PREFETCH
 #define FSP_FWD_PREFETCH 1  // 1: TMEM load of the next 32-column chunk overlaps this chunk's math
 #endif
-#ifndef FSP_FWD_ONEPASS
-#define FSP_FWD_ONEPASS 0  // 1: S row kept in registers between the max and exp passes
-#endif
 #ifndef FSP_POLY_EVERY
 #define FSP_POLY_EVERY 4
 #endif
@@ -514,8 +511,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         printf("fwd MMA issuer cycles (sum over CTAs): tile-steps %llu total %llu | p_half A %llu "
                "p_half B %llu k_full %llu v_full %llu q %llu\n", g_fwd_wait[8], g_fwd_wait[7],
                g_fwd_wait[0], g_fwd_wait[1], g_fwd_wait[2], g_fwd_wait[3], g_fwd_wait[5]);
-        printf("fwd softmax warp (tile A, quad 0): s_full wait %llu busy %llu\n", g_fwd_wait[9],
-               g_fwd_wait[10]);
+        printf("fwd softmax warp (tile A, quad 0): s_full wait %llu busy %llu | to max %llu to "
+               "first-half release %llu\n", g_fwd_wait[9], g_fwd_wait[10], g_fwd_wait[11],
+               g_fwd_wait[12]);
         for (int i = 0; i < 16; ++i) g_fwd_wait[i] = 0;
         g_fwd_done = 0;
       }
@@ -580,26 +578,17 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       const int lim = q_pos - j * 128;  // causal: column c valid iff c <= lim (diagonal tile)
       auto tile_body = [&](auto diag_c) {
         constexpr bool kDiag = decltype(diag_c)::value;
-        // pass 1: row max; four independent FMNMX3 chains.  FSP_FWD_ONEPASS keeps the whole
-        // 128-column row in registers (one TMEM round trip per tile), otherwise chunked
-        // loads are repeated in pass 2.
+        // pass 1: row max; four independent FMNMX3 chains over chunked TMEM loads (the
+        // whole 128-column row does not fit the 168-register budget of 10 warps per CTA)
         float mxs[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#if FSP_FWD_ONEPASS
-        uint32_t row_s[4][32];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_addr + s_col + 32 * c, row_s[c]);
-        tmem_ld_wait();
-#endif
-#if FSP_FWD_PREFETCH && !FSP_FWD_ONEPASS
+#if FSP_FWD_PREFETCH
         uint32_t buf[2][32];  // chunk c+1 is in flight while chunk c is processed
         tmem_ld32(tmem + lane_addr + s_col, buf[0]);
         tmem_ld_wait_tied(buf[0]);
 #endif
 #pragma unroll
         for (int c = 0; c < 128; c += 32) {
-#if FSP_FWD_ONEPASS
-          const uint32_t(&r)[32] = row_s[c / 32];
-#elif FSP_FWD_PREFETCH
+#if FSP_FWD_PREFETCH
           uint32_t(&r)[32] = buf[(c / 32) & 1];
           if (c + 32 < 128) tmem_ld32(tmem + lane_addr + s_col + c + 32, buf[((c / 32) + 1) & 1]);
 #else
@@ -618,11 +607,14 @@ __global__ void __launch_bounds__(kF2Threads, 1)
               }
               mxs[a] = fmax3(mxs[a], v0, v1);
             }
-#if FSP_FWD_PREFETCH && !FSP_FWD_ONEPASS
+#if FSP_FWD_PREFETCH
           if (c + 32 < 128) tmem_ld_wait_tied(buf[((c / 32) + 1) & 1]);
 #endif
         }
         const float mx = fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3]));
+#if FSP_FWD_TIMING
+        if (warp == 2 && lane == 0) atomicAdd(&g_fwd_wait[11], (unsigned long long)(clock64() - ts1));
+#endif
         const float m_new = fmaxf(m, mx * sl2);
         // warp-uniform lazy rescale decision (TMEM access is warp-collective)
         const bool grow = __any_sync(0xffffffffu, m_new > m + 8.f);
@@ -647,16 +639,14 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         // Packed fp32x2 math; one pair in four exponentiates on the FMA pipe (ex2_poly2).
         const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(-m, -m);
         uint64_t sum2[4] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
-#if FSP_FWD_PREFETCH && !FSP_FWD_ONEPASS
+#if FSP_FWD_PREFETCH
         tmem_ld32(tmem + lane_addr + s_col, buf[0]);
         tmem_ld_wait_tied(buf[0]);
 #endif
 #pragma unroll
         for (int c = 0; c < 128; c += 32) {
           uint32_t pk[16];
-#if FSP_FWD_ONEPASS
-          const uint32_t(&r)[32] = row_s[c / 32];
-#elif FSP_FWD_PREFETCH
+#if FSP_FWD_PREFETCH
           uint32_t(&r)[32] = buf[(c / 32) & 1];
           if (c + 32 < 128) tmem_ld32(tmem + lane_addr + s_col + c + 32, buf[((c / 32) + 1) & 1]);
 #else
@@ -693,8 +683,12 @@ __global__ void __launch_bounds__(kF2Threads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_half + 2 * x);
+#if FSP_FWD_TIMING
+            if (warp == 2 && lane == 0)
+              atomicAdd(&g_fwd_wait[12], (unsigned long long)(clock64() - ts1));
+#endif
           }
-#if FSP_FWD_PREFETCH && !FSP_FWD_ONEPASS
+#if FSP_FWD_PREFETCH
           if (c + 32 < 128) tmem_ld_wait_tied(buf[((c / 32) + 1) & 1]);
 #endif
         }
@@ -779,7 +773,8 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
   if (D == 128) {  // schedule entries are 256-row tile pairs (fsp_attn_schedule, head_dim 128)
     const int smem = Fwd2Smem::kBytes + 1024;
-    FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
     attn_fwd_pair_kernel<<<(unsigned)a->n_tiles, kF2Threads, smem, stream>>>(tq, tk, tv, p);
   } else {
     const int smem = FwdSmem<D>::kBytes + 1024;
