@@ -36,26 +36,28 @@ class FlexSPAttention(torch.autograd.Function):
         out, saved = executor.micro_batch_forward(step_plan, mb, qkv)
         ctx.executor, ctx.step_plan, ctx.micro_batch = executor, step_plan, micro_batch
         ctx.shape = qkv_local.shape
-        if out is None:  # this rank holds no group in this micro-batch
-            ctx.saved = None
+        ctx.idle = out is None
+        if ctx.idle:  # this rank holds no group in this micro-batch
             return qkv_local.new_empty((0, executor.n_heads, executor.head_dim))
         out = out.clone()  # the heap region is reused by the next call
+        # save_for_backward (not ctx attributes) so activation checkpointing can drop and
+        # recompute these like any other saved activation
         if mb.in_place:
-            ctx.saved = (qkv, out, saved[2])
+            ctx.save_for_backward(qkv, out, saved[2])
         else:
             recv, o_heads, lse = saved
-            ctx.saved = (recv.clone(), o_heads.clone(), lse)
+            ctx.save_for_backward(recv.clone(), o_heads.clone(), lse)
         return out
 
     @staticmethod
     def backward(ctx, dout: torch.Tensor):
         ex, sp, m = ctx.executor, ctx.step_plan, ctx.micro_batch
         mb = sp.micro_batches[m]
-        if ctx.saved is None:
+        if ctx.idle:
             ex.micro_batch_backward(sp, mb, None, dout)
             return torch.zeros(ctx.shape, dtype=torch.bfloat16, device=dout.device), None, None, None
-        dqkv = ex.micro_batch_backward(sp, mb, ctx.saved, dout.to(torch.bfloat16).contiguous())
-        ctx.saved = None
+        saved = ctx.saved_tensors
+        dqkv = ex.micro_batch_backward(sp, mb, saved, dout.to(torch.bfloat16).contiguous())
         return dqkv.clone(), None, None, None
 
 

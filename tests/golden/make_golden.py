@@ -14,6 +14,8 @@ Outputs (all small JSON/NPZ, committed):
   c3_n{N}_*.json, c4_n{N}_*.json   C3 (13B-shape, H=40) / C4 (30B-shape, H=52) batches
                   planned with the fitted B200 coefficients (`--scale-configs` regenerates
                   only these)
+  c3full_n{N}_*.json  C3 batch planned with full-step (40-layer) coefficients for
+                  scripts/bench_full_step.py (`--full-step` regenerates only these)
   rand_*.json     random small instances (N = 4, 8) for layout parity
   attn_small.npz  attention golden vectors from oracle/attention_ref.py (fp32), checked
                   against torch SDPA when generated
@@ -164,6 +166,32 @@ def scaled_coeffs(heads: int) -> CostCoefficients:
                             m_token=cal["m_token"] * f, m_ms=cal["m_ms"])
 
 
+# C3 full training step (scripts/bench_full_step.py: 40 layers with activation checkpointing,
+# GEMMs + SP attention): coefficients measured on 4xB200 with an 8-layer run of that script
+# (attention 186 ms and GEMMs 107 ms per layer at d=4 for 63,040 tokens per rank):
+# alpha1 = 0.186 s * 4 / sum s^2 per layer x 40 layers; alpha2 = 107 ms / 63,040 tokens x 40;
+# alpha3 = three exchanges (fwd, recompute, bwd) of 4h bf16 per token per layer x 40;
+# m_token = 40 checkpointed layer inputs + one layer's transient activations per token;
+# m_ms = bf16 weights + gradients of 40 layers (12.6 B parameters) + workspaces.
+C3FULL_COEFFS = CostCoefficients(alpha1=1.62e-9, alpha2=6.8e-5, beta1=5e-3, alpha3=4.9e6,
+                                 beta2=2e-3, m_token=7.2e5, m_ms=5.5e10)
+
+
+def make_full_step_plans():
+    b = gen_longtail(32, ("pareto", 1.1, 1024), 131072, seed=0)[0]
+    for n in (2, 4, 8):
+        cl = b200_cluster(n)
+        extra = {"coefficients": C3FULL_COEFFS.to_json_dict(), "cluster": cl.to_json_dict(),
+                 "heads": 40, "layers": 40}
+        p = solve_batch(b, cl, C3FULL_COEFFS, SolveConfig(jobs=8, time_limit=60))
+        dump(f"c3full_n{n}_flexsp.json", plan_doc(p, b, extra))
+        s = plan_static(b, cl, C3FULL_COEFFS, n)
+        dump(f"c3full_n{n}_static.json", plan_doc(s, b, extra))
+        print(f"c3full N={n}: flexsp {p.predicted_total_time:.3f}s "
+              f"{[sorted((g.degree for g in mb.selected_groups), reverse=True) for mb in p.micro_batches]}"
+              f" static {s.predicted_total_time:.3f}s", flush=True)
+
+
 def make_scale_configs():
     for name, spec in SCALE_CONFIGS.items():
         k, dist_, mx = spec["gen"]
@@ -186,5 +214,7 @@ def make_scale_configs():
 if __name__ == "__main__":
     if "--scale-configs" in sys.argv:  # C3 / C4 plans only
         make_scale_configs()
+    elif "--full-step" in sys.argv:  # C3 full-step plans only
+        make_full_step_plans()
     else:
         main()

@@ -72,3 +72,46 @@ def test_layer_matches_fp32_reference():
         _close(xl.grad, xr.grad, 3e-2)
     for name, prm in layer.named_parameters():
         _close(prm.grad, params[name].grad, 3e-2)
+
+
+def test_layer_under_activation_checkpointing():
+    """Two stacked layers wrapped in torch.utils.checkpoint (the full-step benchmark's
+    setting): the attention forward is recomputed inside backward, and outputs / gradients
+    equal the plain autograd run (dQ up to fp32 reduction order)."""
+    from torch.utils.checkpoint import checkpoint
+
+    from paper_2412_01523_b200.executor import FlexSPExecutor
+    from paper_2412_01523_b200.layer import FlexSPTransformerLayer
+    H, D = 2, 128
+    lengths = [300, 1, 130, 700, 64]
+    plan = {"schema": 1, "strategy": "flexsp", "micro_batches": [
+        {"selected_groups": [{"slot_id": 0, "degree": 1, "sequence_indices": [3, 1]}]},
+        {"selected_groups": [{"slot_id": 0, "degree": 1, "sequence_indices": [0, 2, 4]}]}]}
+    ex = FlexSPExecutor(1, 0, H, D, "cuda")
+    sp = ex.prepare(plan, lengths)
+    layers = [FlexSPTransformerLayer(H * D, H, seed=s) for s in (1, 2)]
+    g = torch.Generator().manual_seed(9)
+    T = sum(lengths)
+    x = torch.randn(T, H * D, generator=g).bfloat16()
+    dy = torch.randn(T, H * D, generator=g).bfloat16()
+    results = []
+    for use_ckpt in (False, True):
+        for l in layers:
+            l.zero_grad(set_to_none=True)
+        outs, xgrads = [], []
+        for m, mb in enumerate(sp.micro_batches):
+            tok = torch.from_numpy(mb.local_tokens)
+            h0 = x[tok].cuda().requires_grad_(True)
+            h = h0
+            for l in layers:
+                h = checkpoint(l, h, ex, sp, m, use_reentrant=False) if use_ckpt else l(h, ex, sp, m)
+            h.backward(dy[tok].cuda())
+            outs.append(h.detach().clone())
+            xgrads.append(h0.grad.clone())
+        grads = [p.grad.clone() for l in layers for p in l.parameters()]
+        results.append((outs, xgrads, grads))
+    (o0, x0, g0), (o1, x1, g1) = results
+    for a, b in zip(o0, o1):
+        assert torch.equal(a, b)
+    for a, b in zip(x0 + g0, x1 + g1):
+        _close(b, a.float().cpu(), 1e-2)

@@ -16,7 +16,9 @@ ROOT = Path(__file__).resolve().parent.parent
 CASES = [(2, "c1_flexsp_2tier.json", 8), (2, "c1_static2.json", 8), (4, "rand0_n4_flexsp.json", 8),
          (4, "rand2_n4_flexsp.json", 8), (8, "rand1_n8_flexsp.json", 8),
          # uneven head splits: 5 heads over 2 ranks, 10 over 4
-         (2, "c1_static2.json", 5), (4, "rand0_n4_flexsp.json", 10)]
+         (2, "c1_static2.json", 5), (4, "rand0_n4_flexsp.json", 10),
+         # ranks left idle by a micro-batch (sum of degrees < N)
+         (4, "idle_n4.json", 8)]
 
 
 @pytest.mark.parametrize("n,plan,heads", CASES)
