@@ -112,3 +112,27 @@ def test_numpy_exchange_restatement_roundtrip_uneven_heads():
     back = layout_ref.ulysses_head2seq(heads, M, H, D)
     for a, c in zip(back, shards):
         np.testing.assert_array_equal(a, c)
+
+
+def test_sampled_row_restatement_matches_dense_oracle():
+    """oracle/sampled_ref.py (the full-size checker) == the dense restatement."""
+    from oracle.sampled_ref import key_rows, query_rows
+    g = torch.Generator().manual_seed(21)
+    lens = [257, 40]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T, H, D = int(cu[-1]), 2, 32
+    q, k, v, do = (torch.randn(T, H, D, generator=g).bfloat16() for _ in range(4))
+    o_ref, lse_ref = attention_fwd_ref(q, k, v, cu)
+    dq_ref, dk_ref, dv_ref = attention_bwd_ref(q, k, v, do, cu)
+    s0, s1, h = int(cu[0]), int(cu[1]), 1
+    rows = [0, 1, 100, 256]
+    qr = query_rows(q[s0:s1, h], k[s0:s1, h], v[s0:s1, h], do[s0:s1, h], rows)
+    np.testing.assert_allclose(qr["o"], o_ref[s0:s1, h][rows].numpy(), atol=1e-5)
+    np.testing.assert_allclose(qr["lse"], lse_ref[h, s0:s1][rows].numpy(), atol=1e-5)
+    np.testing.assert_allclose(qr["dq"], dq_ref[s0:s1, h][rows].numpy(), atol=1e-4)
+    all_rows = list(range(s1 - s0))
+    full = query_rows(q[s0:s1, h], k[s0:s1, h], v[s0:s1, h], do[s0:s1, h], all_rows)
+    kr = key_rows(q[s0:s1, h], k[s0:s1, h], v[s0:s1, h], do[s0:s1, h], [0, 7, 256],
+                  full["lse"], full["delta"])
+    np.testing.assert_allclose(kr["dk"], dk_ref[s0:s1, h][[0, 7, 256]].numpy(), atol=1e-4)
+    np.testing.assert_allclose(kr["dv"], dv_ref[s0:s1, h][[0, 7, 256]].numpy(), atol=1e-4)
