@@ -1,6 +1,6 @@
 """Multi-GPU parity of the full SP step (real NVSwitch peer memory), one process per GPU.
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/mgpu_parity.py [plan.json [heads]]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/mgpu_parity.py [plan.json [heads [head_dim]]]
 
 Runs every micro-batch of a reference-planner plan through FlexSPExecutor on N GPUs,
 reassembles O and dQKV in loader order on rank 0 and compares them with the CPU oracle
@@ -35,7 +35,8 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else DEFAULT[world]
     plan = json.loads((ROOT / "tests" / "golden" / name).read_text())
     lengths = plan["lengths"]
-    H, D = (int(sys.argv[2]) if len(sys.argv) > 2 else 8), 128  # H % d != 0: uneven split
+    H = int(sys.argv[2]) if len(sys.argv) > 2 else 8  # H % d != 0: uneven head split
+    D = int(sys.argv[3]) if len(sys.argv) > 3 else 128
     ex = FlexSPExecutor(world, rank, H, D, dev)
     sp = ex.prepare(plan, lengths)
     T = sum(lengths)
@@ -98,7 +99,7 @@ def main():
                 torch.allclose(dq[:, i], r, atol=5e-2, rtol=5e-2))
         degs = [sorted((gg["degree"] for gg in mb["selected_groups"]), reverse=True)
                 for mb in plan["micro_batches"]]
-        print(json.dumps({"plan": name, "world": world, "heads": H, "groups": degs, "tokens": T,
+        print(json.dumps({"plan": name, "world": world, "heads": H, "head_dim": D, "groups": degs, "tokens": T,
                           "o_max": float(e_o.max()), "o_mean": float(e_o.mean()),
                           "grad_max": errs, "autograd_ok": autograd_ok, "ok": ok}), flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)
