@@ -171,6 +171,17 @@ int32_t fsp_attn_schedule(const int32_t* cu_seqlens_host, int32_t n_seq, int32_t
                           int32_t head_dim, int32_t kind, int32_t* tiles_host, int32_t capacity);
 int fsp_attn_fwd(const FspAttnFwd* a, void* stream);
 int fsp_attn_bwd(const FspAttnBwd* a, void* stream);
+/* Bytes of fp32 scratch one fsp_attn_bwd call needs from its caller: dq_accum
+ * [n_heads, total_rows, head_dim] + delta [n_heads, total_rows] (the library never
+ * allocates).  Negative sizes -> FSP_ERR_INVALID. */
+int64_t fsp_attn_bwd_workspace_bytes(int32_t total_rows, int32_t n_heads, int32_t head_dim);
+
+/* ------------------------------------------------------------------ layout check */
+/* Host-side validation of one group member's pack index (or a member's slice of an unpack
+ * table): every entry is -1 (pad row) or a loader-order local row in [0, n_local), and the
+ * non-negative entries hit each local row exactly once.  Returns 0 or FSP_ERR_INVALID
+ * (message in fsp_last_error).  The executor runs it on every table it uploads. */
+int fsp_layout_check(const int32_t* index_host, int64_t n_entries, int64_t n_local);
 
 /* ------------------------------------------------------------------ self-test */
 /* Single 128x128xK UMMA tile through TMA+tcgen05, used by the tests to pin the

@@ -29,7 +29,8 @@ c_float = ctypes.c_float
 EXPORTED = (
     "fsp_abi_version", "fsp_last_error", "fsp_pack_rows", "fsp_unpack_rows",
     "fsp_a2a_seq2head", "fsp_a2a_head2seq", "fsp_group_barrier", "fsp_attn_schedule",
-    "fsp_attn_fwd", "fsp_attn_bwd", "fsp_selftest_umma",
+    "fsp_attn_fwd", "fsp_attn_bwd", "fsp_attn_bwd_workspace_bytes", "fsp_layout_check",
+    "fsp_selftest_umma",
 )
 
 
@@ -88,6 +89,10 @@ def load() -> ctypes.CDLL:
     lib.fsp_attn_schedule.restype = c_i32
     lib.fsp_attn_fwd.argtypes = [ctypes.POINTER(FspAttnFwd), c_vp]
     lib.fsp_attn_bwd.argtypes = [ctypes.POINTER(FspAttnBwd), c_vp]
+    lib.fsp_attn_bwd_workspace_bytes.argtypes = [c_i32, c_i32, c_i32]
+    lib.fsp_attn_bwd_workspace_bytes.restype = c_i64
+    lib.fsp_layout_check.argtypes = [ctypes.POINTER(c_i32), c_i64, c_i64]
+    lib.fsp_layout_check.restype = c_i32
     lib.fsp_selftest_umma.argtypes = [c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]
     for name in EXPORTED:
         if not hasattr(lib, name):

@@ -4,6 +4,8 @@
 #include <mutex>
 #include <string>
 
+#include <vector>
+
 #include "fsp_host.h"
 
 namespace fsp {
@@ -80,3 +82,46 @@ int encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, i
 
 extern "C" int fsp_abi_version(void) { return FSP_ABI_VERSION; }
 extern "C" const char* fsp_last_error(void) { return fsp::g_last_error.c_str(); }
+
+extern "C" int64_t fsp_attn_bwd_workspace_bytes(int32_t total_rows, int32_t n_heads,
+                                                int32_t head_dim) {
+  if (total_rows < 0 || n_heads < 0 || head_dim < 0) {
+    fsp::set_error("negative size");
+    return FSP_ERR_INVALID;
+  }
+  return ((int64_t)n_heads * total_rows * head_dim + (int64_t)n_heads * total_rows) * 4;
+}
+
+extern "C" int fsp_layout_check(const int32_t* index_host, int64_t n_entries, int64_t n_local) {
+  if (n_entries < 0 || n_local < 0 || (n_entries > 0 && index_host == nullptr)) {
+    fsp::set_error("bad layout-check arguments");
+    return FSP_ERR_INVALID;
+  }
+  std::vector<uint8_t> seen((size_t)n_local, 0);
+  int64_t hits = 0;
+  for (int64_t i = 0; i < n_entries; ++i) {
+    const int32_t v = index_host[i];
+    if (v < 0) {
+      if (v != -1) {
+        fsp::set_error("entry %lld is %d (only -1 marks a pad row)", (long long)i, v);
+        return FSP_ERR_INVALID;
+      }
+      continue;
+    }
+    if (v >= n_local) {
+      fsp::set_error("entry %lld = %d outside [0, %lld)", (long long)i, v, (long long)n_local);
+      return FSP_ERR_INVALID;
+    }
+    if (seen[v]) {
+      fsp::set_error("local row %d referenced twice", v);
+      return FSP_ERR_INVALID;
+    }
+    seen[v] = 1;
+    ++hits;
+  }
+  if (hits != n_local) {
+    fsp::set_error("%lld of %lld local rows referenced", (long long)hits, (long long)n_local);
+    return FSP_ERR_INVALID;
+  }
+  return FSP_OK;
+}

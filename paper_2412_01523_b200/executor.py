@@ -143,9 +143,15 @@ class FlexSPExecutor:
                 local = grp.local_tokens(j)
                 rmb = RankMicroBatch(lay, grp, j, int(local.shape[0]), local,
                                      head_begin=head_split(self.n_heads, grp.degree))
-                rmb.pack_index = torch.from_numpy(grp.pack_index(j)).to(self.device)
+                pack = grp.pack_index(j)
+                table = grp.unpack_table()
+                # the tables the kernels index with are validated by the library first
+                ops.layout_check(pack, rmb.n_local)
+                for jj in range(grp.degree):
+                    ops.layout_check(table[jj], int((grp.shard(jj) >= 0).sum()))
+                rmb.pack_index = torch.from_numpy(pack).to(self.device)
                 rmb.unpack_table = torch.from_numpy(
-                    np.ascontiguousarray(grp.unpack_table().reshape(-1))).to(self.device)
+                    np.ascontiguousarray(table.reshape(-1))).to(self.device)
                 if grp.degree == 1:
                     # d = 1: no exchange at all — attention reads q/k/v and writes O / dQKV
                     # in place in the rank's loader-order buffers (each sequence is

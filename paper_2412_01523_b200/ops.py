@@ -149,7 +149,8 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
              dq=None, dk=None, dv=None, dq_accum=None, delta=None):
     """Varlen causal attention backward -> (dq, dk, dv), each [T, H, D] bf16.
 
-    dq_accum (fp32 [T, H, D]) and delta (fp32 [H, T]) are optional reusable workspaces.
+    dq_accum (fp32 [H, T, D]) and delta (fp32 [H, T]) are optional reusable workspaces
+    (fsp_attn_bwd_workspace_bytes gives their combined size).
     """
     _require_cuda(q, k, v, o, dout, lse)
     T, H, D = q.shape
@@ -163,10 +164,11 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
     dq = dq if dq is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
     dk = dk if dk is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
     dv = dv if dv is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
-    dq_acc = dq_accum if dq_accum is not None else torch.empty((T, H, D), dtype=torch.float32,
+    dq_acc = dq_accum if dq_accum is not None else torch.empty((H, T, D), dtype=torch.float32,
                                                                device=dev)
     delta = delta if delta is not None else torch.empty((H, T), dtype=torch.float32, device=dev)
-    if dq_acc.numel() < T * H * D or delta.numel() < H * T:
+    need = capi.load().fsp_attn_bwd_workspace_bytes(T, H, D)
+    if (dq_acc.numel() + delta.numel()) * 4 < need or dq_acc.numel() < T * H * D:
         raise ValueError("attention backward workspace too small")
     a = capi.FspAttnBwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(),
                         lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
@@ -231,3 +233,12 @@ def group_barrier(signal_ptrs, rank: int, slot_base: int, epoch: int) -> None:
     capi.check(capi.load().fsp_group_barrier(_ptr_array(signal_ptrs), len(signal_ptrs), rank,
                                              slot_base, epoch & 0xFFFFFFFF, _stream()))
     LAUNCHES[0] += 1 if len(signal_ptrs) > 1 else 0
+
+
+def layout_check(index, n_local: int) -> None:
+    """C-ABI fsp_layout_check on a host int32 index (pack index or one member's unpack
+    table): raises ValueError unless it maps onto [0, n_local) exactly once (-1 = pad)."""
+    import numpy as np
+    idx = np.ascontiguousarray(np.asarray(index, dtype=np.int32))
+    ptr = idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    capi.check(capi.load().fsp_layout_check(ptr, idx.size, int(n_local)))

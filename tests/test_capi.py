@@ -22,7 +22,8 @@ def lib():
 
 def test_exports_every_declared_symbol(lib):
     header = (ROOT / "include" / "flexsp_b200.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|int32_t|const char\*)\s+(fsp_\w+)\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char\*)\s+(fsp_\w+)\(", header,
+                              re.M))
     assert declared, "no declarations parsed"
     from paper_2412_01523_b200 import capi
     assert declared == set(capi.EXPORTED)
@@ -95,3 +96,37 @@ def test_device_ops_reject_cpu_tensors(lib):
     idx = torch.zeros(4, dtype=torch.int32)
     with pytest.raises(ValueError, match="CUDA"):
         ops.pack_rows(x, idx, x.clone())
+
+
+def test_bwd_workspace_bytes(lib):
+    assert lib.fsp_attn_bwd_workspace_bytes(1000, 8, 128) == (8 * 1000 * 128 + 8 * 1000) * 4
+    assert lib.fsp_attn_bwd_workspace_bytes(0, 8, 128) == 0
+    assert lib.fsp_attn_bwd_workspace_bytes(-1, 8, 128) < 0
+
+
+def test_layout_check_accepts_permutations_and_rejects_the_rest(lib):
+    from paper_2412_01523_b200 import ops
+    ops.layout_check([2, 0, -1, 1], 3)
+    ops.layout_check([], 0)
+    ops.layout_check([-1, -1], 0)
+    for bad, n in (([0, 0, 1], 3), ([0, 3], 2), ([0, 1], 3), ([0, -2, 1], 2)):
+        with pytest.raises(ValueError):
+            ops.layout_check(bad, n)
+
+
+def test_layout_check_on_every_golden_plan(lib):
+    """Every rank's pack index and unpack table of every committed plan passes the
+    library's check (the executor runs the same check before uploading them)."""
+    import json
+    from paper_2412_01523_b200 import ops
+    from paper_2412_01523_b200.layout import build_plan_layouts
+    for path in sorted((ROOT / "tests" / "golden").glob("*.json")):
+        plan = json.loads(path.read_text())
+        if "micro_batches" not in plan or "lengths" not in plan:
+            continue
+        world = plan.get("cluster", {}).get("total_devices") or \
+            len(plan["micro_batches"][0].get("group_selection", [0, 0, 0])) // 2 + 1
+        for lay in build_plan_layouts(plan, plan["lengths"], world):
+            for g in lay.groups:
+                for j in range(g.degree):
+                    ops.layout_check(g.pack_index(j), int((g.shard(j) >= 0).sum()))
