@@ -404,6 +404,9 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
                           // stores instead of dQ reductions, 32 = no dQ stores at all,
                           // 64 = no dQ^T TMEM readout
 #endif
+#ifndef FSP_BWD_RING
+#define FSP_BWD_RING 6  // 64-row Q / dO slots of the TMA ring (6 = three 64-query units)
+#endif
 #ifndef FSP_BWD_DS_TMEM
 #define FSP_BWD_DS_TMEM 1  // dS^T also goes to TMEM so dK += dS^T Q is a TS MMA
 #endif
@@ -423,7 +426,7 @@ constexpr uint32_t kV2ColS = 256, kV2ColDP = 384;
 struct BwdSmemV2 {
   static constexpr int kTileBytes = 128 * 128 * 2;
   static constexpr int kHalfBytes = 64 * 128 * 2;     // one 64-row half of Q_i or dO_i
-  static constexpr int kSlots = 6;                    // 3 half tiles of (Q, dO) in flight
+  static constexpr int kSlots = FSP_BWD_RING;         // Q / dO half tiles in flight
   static constexpr int kK = 0;
   static constexpr int kV = kK + kTileBytes;
   static constexpr int kRing = kV + kTileBytes;
@@ -461,14 +464,16 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   float* delta_s = lse_s + 256;                              // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* bar_kv = bars + 0;
-  uint64_t* ring_full = bars + 1;   // [6]
-  uint64_t* ring_empty = bars + 7;  // [6]
-  uint64_t* s_full = bars + 13;     // [2]
-  uint64_t* p_ready = bars + 15;    // [2]
-  uint64_t* dq_full = bars + 17;    // [2]
-  uint64_t* tm_free = bars + 19;    // [2]
-  uint64_t* acc_done = bars + 21;   // dK / dV final
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  constexpr int kR = L::kSlots;
+  static_assert(1 + 2 * kR + 9 <= 32, "barrier region holds 32 mbarriers");
+  uint64_t* ring_full = bars + 1;            // [kSlots]
+  uint64_t* ring_empty = bars + 1 + kR;      // [kSlots]
+  uint64_t* s_full = bars + 1 + 2 * kR;      // [2]
+  uint64_t* p_ready = s_full + 2;            // [2]
+  uint64_t* dq_full = s_full + 4;            // [2]
+  uint64_t* tm_free = s_full + 6;            // [2]
+  uint64_t* acc_done = s_full + 8;           // dK / dV final
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 9);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
