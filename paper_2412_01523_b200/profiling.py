@@ -16,6 +16,7 @@ class EventTimer:
         self.enabled = False
         self._pending: list[tuple[str, torch.cuda.Event, torch.cuda.Event, float]] = []
         self.work: dict[str, float] = defaultdict(float)
+        self.tag = ""  # appended to every span name (e.g. "@mb1" for a per-micro-batch split)
 
     def start(self):
         self.enabled = True
@@ -39,7 +40,7 @@ class EventTimer:
                 if timer.enabled:
                     e = torch.cuda.Event(enable_timing=True)
                     e.record()
-                    timer._pending.append((name, self_inner.s, e, work))
+                    timer._pending.append((name + timer.tag, self_inner.s, e, work))
                 return False
         return _Span()
 

@@ -31,6 +31,7 @@ sys.path.insert(0, str(ROOT))
 
 from paper_2412_01523_b200.executor import FlexSPExecutor  # noqa: E402
 from paper_2412_01523_b200.layer import FlexSPTransformerLayer  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 HIDDEN, HEADS = 5120, 40
 
@@ -41,7 +42,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--strategy", default="both", choices=["flexsp", "static", "both"])
-    ap.add_argument("--config", default="c3")
+    ap.add_argument("--config", default="c3full")
+    ap.add_argument("--per-mb", action="store_true", help="split the SP-path spans per micro-batch")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -67,6 +69,7 @@ def main():
 
         def step():
             for m in range(len(sp.micro_batches)):
+                ex.timer.tag = f"@mb{m}" if args.per_mb else ""
                 h = xs[m]
                 for layer in layers:
                     h = checkpoint(layer, h, ex, sp, m, use_reentrant=False)
@@ -89,13 +92,17 @@ def main():
         t0 = time.perf_counter()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ex.timer.start()
+        clk = ClockSampler(local)
         s.record()
         for _ in range(args.steps):
             step()
         e.record()
         torch.cuda.synchronize()
         ex.timer.stop()
-        kern = {k: v["ms"] / args.steps for k, v in ex.timer.summary().items()}
+        clocks = clk.stop()
+        kern = {k: {"ms": v["ms"] / args.steps, "launches": v["n"] // args.steps,
+                    "tflops": v["work"] / v["ms"] / 1e9 if v["work"] and v["ms"] else None}
+                for k, v in ex.timer.summary().items()}
         allk = [None] * world
         dist.all_gather_object(allk, kern)
         wall = time.perf_counter() - t0
@@ -103,7 +110,7 @@ def main():
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         tokens = sum(plan["lengths"])
         out[strategy] = {"ms_per_step": float(ms.item()), "tokens_per_s": tokens / (ms.item() / 1e3),
-                         "wall_s_per_step": wall / args.steps,
+                         "wall_s_per_step": wall / args.steps, "clocks_rank0": clocks,
                          "sp_path_ms_per_step_per_rank": allk,
                          "groups_per_micro_batch": [sorted((gg["degree"] for gg in mb["selected_groups"]),
                                                            reverse=True) for mb in plan["micro_batches"]]}
