@@ -347,53 +347,73 @@ class FlexSPExecutor:
                 sink(m, out, dqkv)
 
     def step_from_host(self, sp: StepPlan, host_qkv: Sequence[torch.Tensor],
-                       host_dout: Sequence[torch.Tensor], sink=None) -> torch.Tensor:
+                       host_dout: Sequence[torch.Tensor], sink=None,
+                       prefetch_next: tuple | None = None) -> torch.Tensor:
         """The same step fed straight from pinned host memory (the data-loader path).
 
         Micro-batch m+1's q/k/v and dO are copied host->device on a side stream into the
         other half of a double buffer while micro-batch m computes, so PCIe transfer and
-        the SP step overlap.  Returns a device fp32 scalar, the step's <O, dO> "loss"
-        (a cheap reduction over every output, read back by the caller).
+        the SP step overlap.  `prefetch_next = (next_sp, next_host_qkv, next_host_dout)`
+        also starts the NEXT step's first micro-batch copy while this step's last
+        micro-batch computes (what a data loader does between steps); the next call with
+        those same host tensors then finds it in flight instead of copying again.
+        Returns a device fp32 scalar, the step's <O, dO> "loss" (a cheap reduction over
+        every output, read back by the caller).
         """
         cur = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_h2d_stream"):
             self._h2d_stream = torch.cuda.Stream(self.device)
+            # persistent across calls: a copy must not overwrite a slot the previous step
+            # is still reading (waiting on a never-recorded event is a no-op)
+            self._h2d_consumed = [torch.cuda.Event() for _ in range(2)]
+            self._h2d_loaded = [torch.cuda.Event() for _ in range(2)]
+            self._h2d_slot = 0            # slot the next copy goes to (strictly alternating)
+            self._h2d_prefetched = None   # (host qkv, host dout, slot) of an in-flight copy
         side = self._h2d_stream
+        consumed, loaded = self._h2d_consumed, self._h2d_loaded
         n = len(sp.micro_batches)
         hd = self.n_heads * self.head_dim
-        max_rows = max((mb.n_local for mb in sp.micro_batches), default=0)
-        bufs = []
-        for k in range(2):
-            q = self._workspace(f"h2d_qkv{k}", max(max_rows, 1) * 3 * hd, torch.bfloat16)
-            d = self._workspace(f"h2d_do{k}", max(max_rows, 1) * hd, torch.bfloat16)
-            bufs.append((q, d))
-        loaded = [torch.cuda.Event() for _ in range(2)]
-        # persistent across calls: the next step's first copies must not overwrite a buffer
-        # the previous step is still reading (waiting on a never-recorded event is a no-op)
-        if not hasattr(self, "_h2d_consumed"):
-            self._h2d_consumed = [torch.cuda.Event() for _ in range(2)]
-        consumed = self._h2d_consumed
+        rows_needed = max((mb.n_local for mb in sp.micro_batches), default=0)
+        if prefetch_next is not None and prefetch_next[0].micro_batches:
+            rows_needed = max(rows_needed, prefetch_next[0].micro_batches[0].n_local)
+        rows_needed = max(rows_needed, 1)
+        have = self._ws.get("h2d_do0")
+        if have is None or have.numel() < rows_needed * hd:
+            self._h2d_prefetched = None  # the slots are reallocated: drop an in-flight copy
+            cur.wait_stream(side)
+        bufs = [(self._workspace(f"h2d_qkv{k}", rows_needed * 3 * hd, torch.bfloat16),
+                 self._workspace(f"h2d_do{k}", rows_needed * hd, torch.bfloat16)) for k in range(2)]
         loss = torch.zeros((), dtype=torch.float32, device=self.device)
 
-        def issue_copy(m):
-            k = m & 1
-            rows = sp.micro_batches[m].n_local
+        def issue_copy(hq, hdo, rows) -> int:
+            k = self._h2d_slot
+            self._h2d_slot ^= 1
             with torch.cuda.stream(side):
                 side.wait_event(consumed[k])
                 q, d = bufs[k]
                 if rows:
-                    q[:rows * 3 * hd].view(rows, 3 * hd).copy_(host_qkv[m].view(rows, 3 * hd),
-                                                                 non_blocking=True)
-                    d[:rows * hd].view(rows, hd).copy_(host_dout[m].view(rows, hd),
-                                                       non_blocking=True)
+                    q[:rows * 3 * hd].view(rows, 3 * hd).copy_(hq.view(rows, 3 * hd),
+                                                               non_blocking=True)
+                    d[:rows * hd].view(rows, hd).copy_(hdo.view(rows, hd), non_blocking=True)
                 loaded[k].record(side)
+            return k
 
+        slots: list[int] = []
+        pf, self._h2d_prefetched = self._h2d_prefetched, None
         if n:
-            issue_copy(0)
+            if pf is not None and pf[0] is host_qkv[0] and pf[1] is host_dout[0]:
+                slots.append(pf[2])
+            else:
+                slots.append(issue_copy(host_qkv[0], host_dout[0], sp.micro_batches[0].n_local))
         for m, mb in enumerate(sp.micro_batches):
             if m + 1 < n:
-                issue_copy(m + 1)
-            k = m & 1
+                slots.append(issue_copy(host_qkv[m + 1], host_dout[m + 1],
+                                        sp.micro_batches[m + 1].n_local))
+            elif prefetch_next is not None and prefetch_next[0].micro_batches:
+                nsp, nq, nd = prefetch_next
+                k = issue_copy(nq[0], nd[0], nsp.micro_batches[0].n_local)
+                self._h2d_prefetched = (nq[0], nd[0], k)
+            k = slots[m]
             cur.wait_event(loaded[k])
             rows = mb.n_local
             q = bufs[k][0][:rows * 3 * hd].view(rows, 3, self.n_heads, self.head_dim)

@@ -185,6 +185,44 @@ def test_step_from_host_matches_device_step():
         torch.testing.assert_close(res[("host", m)][1], res[("dev", m)][1], atol=2e-2, rtol=2e-2)
 
 
+def test_step_from_host_prefetch_across_steps():
+    """prefetch_next: the next step's first micro-batch is copied during this step's last
+    one; consecutive steps with different inputs (and an odd micro-batch count, so the
+    double-buffer slots alternate across steps) still compute exactly the device step,
+    and a prefetch for other host tensors than the next call's is ignored."""
+    from paper_2412_01523_b200.executor import FlexSPExecutor
+    H, D = 4, 128
+    lengths = [700, 1, 130, 2048, 64, 300]
+    plan = _plan_n1(lengths, [[3], [1, 5, 0], [2, 4]])
+    ex = FlexSPExecutor(1, 0, H, D, "cuda")
+    sp = ex.prepare(plan, lengths)
+    T = sum(lengths)
+    toks = [torch.from_numpy(mb.local_tokens) for mb in sp.micro_batches]
+    inputs, ref = [], []
+    for seed in range(3):
+        g = torch.Generator().manual_seed(20 + seed)
+        qkv = torch.randn(T, 3, H, D, generator=g).bfloat16()
+        dout = torch.randn(T, H, D, generator=g).bfloat16()
+        outs = {}
+        ex.step(sp, [qkv[t].cuda() for t in toks], [dout[t].cuda() for t in toks],
+                sink=lambda m, o, dq, outs=outs: outs.__setitem__(m, (o.float().cpu(), dq.float().cpu())))
+        ref.append(outs)
+        inputs.append(([qkv[t].contiguous().pin_memory() for t in toks],
+                       [dout[t].contiguous().pin_memory() for t in toks]))
+    # steps 0 -> 1 -> 2 prefetching the right next inputs, then step 0 after a prefetch of
+    # step 1's tensors (mismatch: must copy its own)
+    order = [(0, 1), (1, 2), (2, 1), (0, None)]
+    for i, nxt in order:
+        got = {}
+        pre = None if nxt is None else (sp, inputs[nxt][0], inputs[nxt][1])
+        ex.step_from_host(sp, inputs[i][0], inputs[i][1], prefetch_next=pre,
+                          sink=lambda m, o, dq, got=got: got.__setitem__(m, (o.float().cpu(), dq.float().cpu())))
+        torch.cuda.synchronize()
+        for m in range(len(toks)):
+            torch.testing.assert_close(got[m][0], ref[i][m][0])
+            torch.testing.assert_close(got[m][1], ref[i][m][1], atol=2e-2, rtol=2e-2)
+
+
 def test_flexsp_attention_autograd_two_layers():
     """FlexSPAttention.apply through torch autograd: two layers' forwards of every
     micro-batch run before any backward (so the heap regions are reused in between), and
