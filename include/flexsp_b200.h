@@ -41,7 +41,7 @@ extern "C" {
 #define FSP_ERR_CUDA (-2)
 #define FSP_ERR_UNSUPPORTED (-3)
 
-#define FSP_ABI_VERSION 3
+#define FSP_ABI_VERSION 4
 
 int fsp_abi_version(void);
 const char* fsp_last_error(void);
@@ -105,6 +105,30 @@ int fsp_group_barrier(uint32_t* const* peer_signal, int32_t degree, int32_t rank
                       int32_t slot_base, uint32_t epoch, void* stream);
 
 /* ------------------------------------------------------------------ attention */
+/* Fused head->seq exchange (Eq. 4) in an attention epilogue (ABI 4).
+ * When degree > 0 the kernel stores every output row t of the group-packed sequence (its
+ * own row index, 0 <= t < degree*rows_per_rank) for its heads ALSO into group member
+ * r = t / rows_per_rank's sequence-sharded buffer peer_dst[r] (mapped into this process,
+ * rows of n_mats matrices: matrix m of destination row u starts at element
+ * u*dst_stride + m*mat_stride) at row d_unpack[t] (< 0: pad row, dropped) and heads
+ * [head_offset, head_offset + n_heads).  d_unpack is the group's unpack table
+ * ([degree][rows_per_rank], the one fsp_a2a_head2seq takes), so one fused launch does
+ * what the attention launch followed by fsp_a2a_head2seq does, with the NVLink stores
+ * issued tile by tile while other tiles still compute.  The caller still closes the
+ * exchange with fsp_group_barrier.  Forward: O is matrix 0 (o is still written locally,
+ * the backward needs it).  Backward: dQ, dK, dV are matrices 0, 1, 2 and the local
+ * dq / dk / dv pointers may be NULL. */
+typedef struct FspHeadScatter {
+  int32_t degree;          /* 0 = off; else 1..8 */
+  int32_t rows_per_rank;   /* R */
+  int32_t head_offset;     /* first head of this member in the destination rows */
+  int32_t reserved;
+  int64_t dst_stride;      /* elements between destination rows */
+  int64_t mat_stride;      /* elements between the matrices of one destination row */
+  const int32_t* d_unpack; /* device [degree * rows_per_rank] */
+  void* peer_dst[8];       /* member r's destination base, peer-mapped */
+} FspHeadScatter;
+
 /* Varlen causal attention over cu_seqlens-packed sequences (flash-attn varlen
  * semantics: causal inside each sequence, no cross-sequence attention, scale
  * default 1/sqrt(head_dim)).  head_dim must be 64 or 128.
@@ -132,6 +156,7 @@ typedef struct FspAttnFwd {
   int32_t n_heads;
   int32_t head_dim;
   float softmax_scale;
+  FspHeadScatter scatter; /* ABI 4: optional fused head->seq of O (degree 0 = off) */
 } FspAttnFwd;
 
 typedef struct FspAttnBwd {
@@ -156,6 +181,7 @@ typedef struct FspAttnBwd {
   int32_t n_heads;
   int32_t head_dim;
   float softmax_scale;
+  FspHeadScatter scatter; /* ABI 4: optional fused head->seq of dQ/dK/dV (degree 0 = off) */
 } FspAttnBwd;
 
 /* CTA schedule: writes n entries of two int32 {seq << 16 | unit, head} to tiles_host

@@ -17,6 +17,7 @@ FSP_OK = 0
 FSP_ERR_INVALID = -1
 FSP_ERR_CUDA = -2
 FSP_ERR_UNSUPPORTED = -3
+ABI_VERSION = 4
 FSP_SCHED_FWD = 0
 FSP_SCHED_BWD = 1
 
@@ -40,12 +41,20 @@ class FspA2A(ctypes.Structure):
                 ("src_stride", c_i64), ("dst_stride", c_i64), ("head_begin", c_i32 * 9)]
 
 
+class FspHeadScatter(ctypes.Structure):
+    """Fused head->seq exchange of an attention output (ABI 4); degree 0 = off."""
+    _fields_ = [("degree", c_i32), ("rows_per_rank", c_i32), ("head_offset", c_i32),
+                ("reserved", c_i32), ("dst_stride", c_i64), ("mat_stride", c_i64),
+                ("d_unpack", c_vp), ("peer_dst", c_vp * 8)]
+
+
 class FspAttnFwd(ctypes.Structure):
     _fields_ = [("q", c_vp), ("k", c_vp), ("v", c_vp), ("o", c_vp), ("lse", c_vp),
                 ("q_stride", c_i64), ("k_stride", c_i64), ("v_stride", c_i64),
                 ("o_stride", c_i64), ("d_cu_seqlens", c_vp), ("d_seq_starts", c_vp),
                 ("d_tiles", c_vp), ("n_tiles", c_i32), ("n_seq", c_i32), ("total_rows", c_i32),
-                ("n_heads", c_i32), ("head_dim", c_i32), ("softmax_scale", c_float)]
+                ("n_heads", c_i32), ("head_dim", c_i32), ("softmax_scale", c_float),
+                ("scatter", FspHeadScatter)]
 
 
 class FspAttnBwd(ctypes.Structure):
@@ -56,7 +65,8 @@ class FspAttnBwd(ctypes.Structure):
                 ("dk_stride", c_i64), ("dv_stride", c_i64), ("dq_accum", c_vp),
                 ("delta", c_vp), ("d_cu_seqlens", c_vp), ("d_seq_starts", c_vp), ("d_tiles", c_vp),
                 ("n_tiles", c_i32), ("n_seq", c_i32), ("total_rows", c_i32),
-                ("n_heads", c_i32), ("head_dim", c_i32), ("softmax_scale", c_float)]
+                ("n_heads", c_i32), ("head_dim", c_i32), ("softmax_scale", c_float),
+                ("scatter", FspHeadScatter)]
 
 
 class FspError(RuntimeError):
@@ -97,7 +107,7 @@ def load() -> ctypes.CDLL:
     for name in EXPORTED:
         if not hasattr(lib, name):
             raise FspError(f"{path} does not export {name}")
-    if lib.fsp_abi_version() != 3:
+    if lib.fsp_abi_version() != ABI_VERSION:
         raise FspError("ABI version mismatch")
     _lib = lib
     return lib

@@ -20,6 +20,7 @@
 
 #include "fsp_host.h"
 #include "fsp_ptx.cuh"
+#include "fsp_scatter.cuh"
 
 namespace fsp {
 
@@ -50,6 +51,7 @@ struct BwdParams {
   int32_t n_heads;
   float scale;
   float scale_log2;
+  ScatterDev sc;  // fused head->seq of dK / dV (matrices 1, 2); sc.degree == 0: off
 };
 
 template <int D>
@@ -75,7 +77,7 @@ template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                    const BwdParams p) {
+                    const __grid_constant__ BwdParams p) {
   using L = BwdSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
@@ -286,8 +288,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ---- epilogue: dK (scaled), dV for kv row r (TMEM loads are warp-collective)
     {
       const bool kvalid = kv_pos < seqlen;
-      __nv_bfloat16* dk_row = p.dk + (int64_t)(seq_start + kv_pos) * p.dk_stride + (int64_t)head * D;
-      __nv_bfloat16* dv_row = p.dv + (int64_t)(seq_start + kv_pos) * p.dv_stride + (int64_t)head * D;
+      // local rows (optional when the exchange is fused) and the fused head->seq
+      // destinations in the owning member's sequence shard (matrices 1 = dK, 2 = dV)
+      const int64_t trow = (int64_t)(seq_start + kv_pos);
+      __nv_bfloat16* dk_row = p.dk ? p.dk + trow * p.dk_stride + (int64_t)head * D : nullptr;
+      __nv_bfloat16* dv_row = p.dv ? p.dv + trow * p.dv_stride + (int64_t)head * D : nullptr;
+      __nv_bfloat16* pk_row = kvalid ? scatter_row(p.sc, trow, 1, head, D) : nullptr;
+      __nv_bfloat16* pv_row = pk_row ? pk_row + p.sc.mat_stride : nullptr;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t a[32], b[32];
@@ -306,8 +313,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           vv.y = pack_bf16(__uint_as_float(b[i + 2]), __uint_as_float(b[i + 3]));
           vv.z = pack_bf16(__uint_as_float(b[i + 4]), __uint_as_float(b[i + 5]));
           vv.w = pack_bf16(__uint_as_float(b[i + 6]), __uint_as_float(b[i + 7]));
-          *reinterpret_cast<uint4*>(dk_row + c + i) = vk;
-          *reinterpret_cast<uint4*>(dv_row + c + i) = vv;
+          if (dk_row) *reinterpret_cast<uint4*>(dk_row + c + i) = vk;
+          if (dv_row) *reinterpret_cast<uint4*>(dv_row + c + i) = vv;
+          if (pk_row) {
+            *reinterpret_cast<uint4*>(pk_row + c + i) = vk;
+            *reinterpret_cast<uint4*>(pv_row + c + i) = vv;
+          }
         }
       }
     }
@@ -365,7 +376,8 @@ template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restrict__ dq_accum,
                                                             __nv_bfloat16* __restrict__ dq,
                                                             int64_t dq_stride, int total_rows,
-                                                            int n_heads, float scale) {
+                                                            int n_heads, float scale,
+                                                            const __grid_constant__ ScatterDev sc) {
   constexpr int kPerRow = D / 8;
   const int64_t n = (int64_t)total_rows * n_heads * kPerRow;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
@@ -382,7 +394,10 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
     v.y = pack_bf16(a.z * scale, a.w * scale);
     v.z = pack_bf16(b.x * scale, b.y * scale);
     v.w = pack_bf16(b.z * scale, b.w * scale);
-    *reinterpret_cast<uint4*>(dq + t * dq_stride + (int64_t)h * D + c) = v;
+    if (dq) *reinterpret_cast<uint4*>(dq + t * dq_stride + (int64_t)h * D + c) = v;
+    // fused head->seq of dQ (matrix 0) into the owning member's sequence shard
+    __nv_bfloat16* prow = scatter_row(sc, t, 0, h, D);
+    if (prow) *reinterpret_cast<uint4*>(prow + c) = v;
   }
 }
 
@@ -455,7 +470,7 @@ __device__ unsigned int g_bwd_done;
 __global__ void __launch_bounds__(kV2Threads, 1)
     attn_bwd_kernel_v2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                       const BwdParams p) {
+                       const __grid_constant__ BwdParams p) {
   constexpr int D = 128;
   using L = BwdSmemV2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -764,12 +779,57 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     // ---- epilogue: this thread writes D/kCW columns of dK (scaled) and dV for kv row r
     if (n_u > 0) mbar_wait(acc_done, 0);  // all MMAs done
     tc_fence_after();
-    {
-      const bool kvalid = kv_pos < seqlen;
-      __nv_bfloat16* dk_row = p.dk + (int64_t)(seq_start + kv_pos) * p.dk_stride + (int64_t)head * D;
-      __nv_bfloat16* dv_row = p.dv + (int64_t)(seq_start + kv_pos) * p.dv_stride + (int64_t)head * D;
+    constexpr int kEpi = D / (kV2Compute / 4);  // dK/dV columns per compute thread
+    const bool kvalid = kv_pos < seqlen;
+    if (p.sc.degree) {
+      // Fused head->seq (Eq. 4) of dK / dV (destination matrices 1 / 2).  A row's columns
+      // are spread over 4 warps, and per-thread 16-byte stores would cross NVLink as
+      // scattered small packets, so the tile is staged in shared memory (the Q/dO ring,
+      // idle after acc_done; 16-byte chunks XOR-swizzled by row) and written back two full
+      // 256-byte rows per warp instruction.
+      uint8_t* stage = smem + L::kRing;  // dK rows [0, 32 KB), dV rows [32 KB, 64 KB)
+      for (int c = ch * kEpi; c < ch * kEpi + kEpi; c += 32) {
+        uint32_t a[32], b[32];
+        tmem_ld32(tmem + lane_addr + kColDK + c, a);
+        tmem_ld32(tmem + lane_addr + kColDV + c, b);
+        tmem_ld_wait();
 #pragma unroll
-      constexpr int kEpi = D / (kV2Compute / 4);  // dK/dV columns per compute thread
+        for (int i = 0; i < 32; i += 8) {
+          uint4 vk, vv;
+          vk.x = pack_bf16(__uint_as_float(a[i]) * p.scale, __uint_as_float(a[i + 1]) * p.scale);
+          vk.y = pack_bf16(__uint_as_float(a[i + 2]) * p.scale, __uint_as_float(a[i + 3]) * p.scale);
+          vk.z = pack_bf16(__uint_as_float(a[i + 4]) * p.scale, __uint_as_float(a[i + 5]) * p.scale);
+          vk.w = pack_bf16(__uint_as_float(a[i + 6]) * p.scale, __uint_as_float(a[i + 7]) * p.scale);
+          vv.x = pack_bf16(__uint_as_float(b[i]), __uint_as_float(b[i + 1]));
+          vv.y = pack_bf16(__uint_as_float(b[i + 2]), __uint_as_float(b[i + 3]));
+          vv.z = pack_bf16(__uint_as_float(b[i + 4]), __uint_as_float(b[i + 5]));
+          vv.w = pack_bf16(__uint_as_float(b[i + 6]), __uint_as_float(b[i + 7]));
+          const int chunk = ((c + i) >> 3) ^ (r & 15);
+          *reinterpret_cast<uint4*>(stage + r * 256 + chunk * 16) = vk;
+          *reinterpret_cast<uint4*>(stage + 32768 + r * 256 + chunk * 16) = vv;
+        }
+      }
+      named_bar_sync(1, 32 * kV2Compute);  // every compute warp's columns are staged
+      const int chunk = lane & 15;
+      for (int pr = cw; pr < 128; pr += kV2Compute) {  // 64 row pairs of dK, then of dV
+        const int mat = pr >> 6;
+        const int srow = 2 * (pr & 63) + (lane >> 4);
+        if (kv0 + srow >= seqlen) continue;
+        const uint4 v = *reinterpret_cast<const uint4*>(stage + mat * 32768 + srow * 256 +
+                                                        ((chunk ^ (srow & 15)) * 16));
+        const int64_t t = seq_start + kv0 + srow;
+        __nv_bfloat16* local = mat ? p.dv : p.dk;
+        if (local)
+          *reinterpret_cast<uint4*>(local + t * (mat ? p.dv_stride : p.dk_stride) +
+                                    (int64_t)head * D + chunk * 8) = v;
+        __nv_bfloat16* prow = scatter_row(p.sc, t, 1 + mat, head, D);
+        if (prow) *reinterpret_cast<uint4*>(prow + chunk * 8) = v;
+      }
+    } else {
+      const int64_t trow = (int64_t)(seq_start + kv_pos);
+      __nv_bfloat16* dk_row = p.dk + trow * p.dk_stride + (int64_t)head * D;
+      __nv_bfloat16* dv_row = p.dv + trow * p.dv_stride + (int64_t)head * D;
+#pragma unroll
       for (int c = ch * kEpi; c < ch * kEpi + kEpi; c += 32) {
         uint32_t a[32], b[32];
         tmem_ld32(tmem + lane_addr + kColDK + c, a);
@@ -870,6 +930,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
 template <int D>
 int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
   const int T = a->total_rows, H = a->n_heads;
+  ScatterDev sc;
+  if (int rc = scatter_from_abi(a->scatter, 3, H, D, T, &sc)) return rc;
   {
     const int64_t warps = (int64_t)T * H;
     int64_t blocks = (warps * 32 + 255) / 256;
@@ -903,6 +965,7 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     p.n_heads = H;
     p.scale = a->softmax_scale;
     p.scale_log2 = a->softmax_scale * kLog2e;
+    p.sc = sc;
     const int64_t grid = a->n_tiles;
     if (D == 128) {
       const int smem = BwdSmemV2::kBytes + 1024;
@@ -922,7 +985,7 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     if (n > 0) {
       attn_bwd_post_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(
           a->dq_accum, reinterpret_cast<__nv_bfloat16*>(a->dq), a->dq_stride, T, H,
-          a->softmax_scale);
+          a->softmax_scale, sc);
       FSP_LAUNCH_CHECK();
     }
   }
@@ -939,8 +1002,9 @@ extern "C" int fsp_attn_bwd(const FspAttnBwd* a, void* stream) {
                              a->d_cu_seqlens, a->d_tiles, a->n_tiles, a->n_seq, a->total_rows,
                              a->n_heads, a->head_dim);
   if (rc) return rc;
-  FSP_CHECK_ARG(a->o && a->dout && a->lse && a->dq && a->dk && a->dv && a->dq_accum && a->delta,
-                "null pointer argument");
+  FSP_CHECK_ARG(a->o && a->dout && a->lse && a->dq_accum && a->delta, "null pointer argument");
+  FSP_CHECK_ARG((a->dq && a->dk && a->dv) || a->scatter.degree > 0,
+                "dq / dk / dv may be NULL only when the head->seq exchange is fused");
   const int64_t hd = (int64_t)a->n_heads * a->head_dim;
   FSP_CHECK_ARG(a->o_stride >= hd && a->do_stride >= hd && a->dq_stride >= hd &&
                     a->dk_stride >= hd && a->dv_stride >= hd,

@@ -17,6 +17,7 @@
 
 #include "fsp_host.h"
 #include "fsp_ptx.cuh"
+#include "fsp_scatter.cuh"
 
 namespace fsp {
 namespace {
@@ -36,6 +37,7 @@ struct FwdParams {
   int32_t total_rows;
   int32_t n_heads;
   float scale_log2;
+  ScatterDev sc;  // fused head->seq of O (sc.degree == 0: off)
 };
 
 template <int D>
@@ -52,7 +54,7 @@ struct FwdSmem {
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ FwdParams p) {
   using L = FwdSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
@@ -252,6 +254,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const float inv_l = 1.f / l;
     const bool valid = q_pos < seqlen;
     __nv_bfloat16* orow = p.o + (int64_t)(seq_start + q_pos) * p.o_stride + (int64_t)head * D;
+    // fused head->seq (Eq. 4): the same row also goes to its owner's sequence shard
+    __nv_bfloat16* prow = valid ? scatter_row(p.sc, seq_start + q_pos, 0, head, D) : nullptr;
 #pragma unroll
     for (int c = 0; c < D; c += 32) {
       uint32_t r[32];
@@ -266,6 +270,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
           v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
           *reinterpret_cast<uint4*>(orow + c + i) = v;
+          if (prow) *reinterpret_cast<uint4*>(prow + c + i) = v;
         }
       }
     }
@@ -347,7 +352,7 @@ __device__ unsigned int g_fwd_done;
 __global__ void __launch_bounds__(kF2Threads, 1)
     attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
-                         const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ FwdParams p) {
   constexpr int D = 128;
   using L = Fwd2Smem;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -714,13 +719,18 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       tc_fence_after();
       const float inv_l = 1.f / l;
       const bool valid = q_pos < seqlen;
-      __nv_bfloat16* orow = p.o + (int64_t)(seq_start + q_pos) * p.o_stride + (int64_t)head * D;
+      if (p.sc.degree) {
+        // Fused head->seq (Eq. 4): O goes to its owner's sequence shard over NVLink as well
+        // as to the local buffer.  One-row-per-thread 16-byte stores would cross NVLink as
+        // 32 scattered 16-byte packets per warp instruction, so the warp first stages its
+        // 32 rows in shared memory (this tile's Q buffer, idle once o_done has fired; 16-byte
+        // chunks XOR-swizzled by row) and then writes two full 256-byte rows per instruction.
+        uint8_t* stage = smem + (x ? L::kQB : L::kQA);
 #pragma unroll
-      for (int c = 0; c < D; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_addr + o_col + c, r);
-        tmem_ld_wait();
-        if (valid) {
+        for (int c = 0; c < D; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_addr + o_col + c, r);
+          tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; i += 8) {
             uint4 v;
@@ -728,7 +738,42 @@ __global__ void __launch_bounds__(kF2Threads, 1)
             v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
             v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
             v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(orow + c + i) = v;
+            const int chunk = ((c + i) >> 3) ^ (row & 15);
+            *reinterpret_cast<uint4*>(stage + row * 256 + chunk * 16) = v;
+          }
+        }
+        __syncwarp();
+        const int chunk = lane & 15;
+#pragma unroll 4
+        for (int rr = 0; rr < 32; rr += 2) {
+          const int srow = quad * 32 + rr + (lane >> 4);  // tile row
+          const int qp = q0 + x * 128 + srow;
+          if (qp >= seqlen) continue;
+          const uint4 v = *reinterpret_cast<const uint4*>(stage + srow * 256 +
+                                                          ((chunk ^ (srow & 15)) * 16));
+          const int64_t t = seq_start + qp;
+          *reinterpret_cast<uint4*>(p.o + t * p.o_stride + (int64_t)head * D + chunk * 8) = v;
+          __nv_bfloat16* prow = scatter_row(p.sc, t, 0, head, D);
+          if (prow) *reinterpret_cast<uint4*>(prow + chunk * 8) = v;
+        }
+      } else {
+        __nv_bfloat16* orow =
+            p.o + (int64_t)(seq_start + q_pos) * p.o_stride + (int64_t)head * D;
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_addr + o_col + c, r);
+          tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint4 v;
+              v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
+              v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+              v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
+              v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
+              *reinterpret_cast<uint4*>(orow + c + i) = v;
+            }
           }
         }
       }
@@ -771,6 +816,7 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   p.total_rows = a->total_rows;
   p.n_heads = a->n_heads;
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  if ((rc = scatter_from_abi(a->scatter, 1, a->n_heads, D, a->total_rows, &p.sc))) return rc;
   if (D == 128) {  // schedule entries are 256-row tile pairs (fsp_attn_schedule, head_dim 128)
     const int smem = Fwd2Smem::kBytes + 1024;
     FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -862,6 +908,11 @@ extern "C" int fsp_attn_fwd(const FspAttnFwd* a, void* stream) {
   FSP_CHECK_ARG(a->o && a->lse, "null output pointer");
   FSP_CHECK_ARG(a->o_stride >= (int64_t)a->n_heads * a->head_dim && a->o_stride % 8 == 0,
                 "bad o_stride");
+  {
+    ScatterDev sc;  // validated before any device work
+    if ((rc = scatter_from_abi(a->scatter, 1, a->n_heads, a->head_dim, a->total_rows, &sc)))
+      return rc;
+  }
   if (a->n_tiles == 0 || a->total_rows == 0) return FSP_OK;
   return a->head_dim == 128 ? launch_fwd<128>(a, (cudaStream_t)stream)
                             : launch_fwd<64>(a, (cudaStream_t)stream);

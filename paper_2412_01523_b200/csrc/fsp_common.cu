@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "fsp_host.h"
+#include "fsp_scatter.cuh"
 
 namespace fsp {
 
@@ -125,3 +126,37 @@ extern "C" int fsp_layout_check(const int32_t* index_host, int64_t n_entries, in
   }
   return FSP_OK;
 }
+
+namespace fsp {
+
+int scatter_from_abi(const FspHeadScatter& a, int n_mats, int n_heads, int head_dim,
+                     int total_rows, ScatterDev* out) {
+  *out = ScatterDev{};
+  if (a.degree == 0) return FSP_OK;
+  FSP_CHECK_ARG(a.degree >= 1 && a.degree <= 8, "scatter degree must be in 1..8 (got %d)",
+                a.degree);
+  FSP_CHECK_ARG(a.rows_per_rank >= 1, "scatter rows_per_rank must be >= 1");
+  FSP_CHECK_ARG((int64_t)a.degree * a.rows_per_rank == total_rows,
+                "scatter: degree * rows_per_rank (%lld) must equal total_rows (%d)",
+                (long long)a.degree * a.rows_per_rank, total_rows);
+  FSP_CHECK_ARG(a.d_unpack != nullptr, "scatter: null unpack table");
+  FSP_CHECK_ARG(a.head_offset >= 0, "scatter: negative head_offset");
+  FSP_CHECK_ARG(a.mat_stride >= 0 && a.mat_stride % 8 == 0 && a.dst_stride % 8 == 0 &&
+                    a.dst_stride >= (n_mats - 1) * a.mat_stride +
+                                       (int64_t)(a.head_offset + n_heads) * head_dim,
+                "scatter: destination strides must cover the heads and be multiples of 8");
+  out->degree = a.degree;
+  out->rows_per_rank = a.rows_per_rank;
+  out->head_offset = a.head_offset;
+  out->dst_stride = a.dst_stride;
+  out->mat_stride = a.mat_stride;
+  out->unpack = a.d_unpack;
+  for (int r = 0; r < a.degree; ++r) {
+    FSP_CHECK_ARG(a.peer_dst[r] != nullptr && ((uintptr_t)a.peer_dst[r] & 15) == 0,
+                  "scatter: destination %d is null or not 16-byte aligned", r);
+    out->dst[r] = reinterpret_cast<__nv_bfloat16*>(a.peer_dst[r]);
+  }
+  return FSP_OK;
+}
+
+}  // namespace fsp

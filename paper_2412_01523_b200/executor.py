@@ -114,7 +114,7 @@ class FlexSPExecutor:
 
     def __init__(self, world_size: int, rank: int, n_heads: int, head_dim: int,
                  device: torch.device | str = "cuda", softmax_scale: float | None = None,
-                 group=None):
+                 group=None, fuse_head2seq: bool = True):
         if head_dim not in (64, 128):
             raise ValueError("head_dim must be 64 or 128")
         self.world_size = world_size
@@ -128,6 +128,10 @@ class FlexSPExecutor:
         self.epoch = 0
         self._ws: dict[str, torch.Tensor] = {}
         self.timer = EventTimer()
+        # Eq. (4) fused into the attention epilogues (O in the forward, dQ/dK/dV in the
+        # backward go straight to their owners' sequence shards); False = separate
+        # fsp_a2a_head2seq launches after attention (kept for A/B measurements)
+        self.fuse_head2seq = fuse_head2seq
 
     # ------------------------------------------------------------ planning -> tables
     def prepare(self, plan: Any, lengths: Sequence[int]) -> StepPlan:
@@ -264,10 +268,18 @@ class FlexSPExecutor:
             self._a2a_qkv(sp, mb, qkv_local, grp, R, hm)
             self._barrier(ranks, self._next_epoch())
         o_heads = self._workspace("o_heads", T * hm * D, torch.bfloat16).view(T, hm, D)
+        out_local, _ = self.local_buffers(sp, mb)
+        scatter = None
+        if self.fuse_head2seq:  # Eq. (4) inside the attention epilogue
+            scatter = ops.HeadScatter(d, R, hb[j], H * D, 0, mb.unpack_table,
+                                      [self.heap.peer(r, off["out_local"]) for r in ranks])
         with self.timer.span("attn_fwd", mb.fwd_flops):
             _, lse = ops.attn_fwd(recv[:, 0, :hn], recv[:, 1, :hn], recv[:, 2, :hn], mb.sched,
-                                  self.scale, out=o_heads[:, :hn])
-        out_local, _ = self.local_buffers(sp, mb)
+                                  self.scale, out=o_heads[:, :hn], scatter=scatter)
+        if scatter is not None:
+            self.timer.count("head2seq_fused", sent_out)  # NVLink bytes inside attn_fwd
+            self._barrier(ranks, self._next_epoch(), "fused_barrier")
+            return out_local, (recv[:, :, :hn], o_heads[:, :hn], lse)
         with self.timer.span("a2a", sent_out):
             ops.a2a("head2seq", o_heads.view(T, hm * D),
                     [self.heap.peer(r, off["out_local"]) for r in ranks], degree=d, rank=j,
@@ -320,9 +332,19 @@ class FlexSPExecutor:
                     rows_per_rank=R, n_mats=1, n_heads=H, head_dim=D, dst_stride=hm * D,
                     index=mb.pack_index, head_begin=hb)
             self._barrier(ranks, self._next_epoch())
-        dqkv_heads = self._workspace("dqkv_heads", T * 3 * hm * D, torch.bfloat16).view(T, 3, hm, D)
         dq_acc = self._workspace("dq_accum", T * hn * D, torch.float32)
         delta = self._workspace("delta", hn * T, torch.float32)
+        if self.fuse_head2seq:  # Eq. (4) for dQ/dK/dV inside the backward's epilogues
+            _, dqkv_local = self.local_buffers(sp, mb)
+            scatter = ops.HeadScatter(d, R, hb[j], 3 * H * D, H * D, mb.unpack_table,
+                                      [self.heap.peer(r, off["dqkv_local"]) for r in ranks])
+            with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
+                ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, do_recv[:, :hn], lse,
+                             mb.sched, self.scale, dq_accum=dq_acc, delta=delta, scatter=scatter)
+            self.timer.count("head2seq_fused", 3 * sent_out)  # NVLink bytes inside attn_bwd
+            self._barrier(ranks, self._next_epoch(), "fused_barrier")
+            return dqkv_local
+        dqkv_heads = self._workspace("dqkv_heads", T * 3 * hm * D, torch.bfloat16).view(T, 3, hm, D)
         with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
             ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, do_recv[:, :hn], lse,
                          mb.sched, self.scale, dq=dqkv_heads[:, 0, :hn], dk=dqkv_heads[:, 1, :hn],

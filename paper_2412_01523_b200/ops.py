@@ -116,6 +116,33 @@ class AttnSchedule:
                             n_heads, head_dim, rows, int(lens.max()) if n_seq else 0, starts)
 
 
+@dataclass
+class HeadScatter:
+    """Fused head->seq exchange (Eq. 4) for an attention launch (C-ABI FspHeadScatter):
+    output row t of the group-packed sequence also lands in member t // rows_per_rank's
+    sequence-sharded buffer `peer_ptrs[member]` at row unpack[t], heads from
+    `head_offset` on; matrices of a destination row are `mat_stride` elements apart."""
+    degree: int
+    rows_per_rank: int
+    head_offset: int
+    dst_stride: int
+    mat_stride: int
+    unpack: torch.Tensor   # int32 [degree * rows_per_rank] device
+    peer_ptrs: list
+
+    def to_c(self) -> "capi.FspHeadScatter":
+        _require_cuda(self.unpack)
+        if self.unpack.dtype != torch.int32 or self.unpack.numel() != self.degree * self.rows_per_rank:
+            raise ValueError("scatter unpack table must be int32 [degree * rows_per_rank]")
+        if len(self.peer_ptrs) != self.degree:
+            raise ValueError("scatter needs one destination pointer per group member")
+        c = capi.FspHeadScatter(self.degree, self.rows_per_rank, self.head_offset, 0,
+                                self.dst_stride, self.mat_stride, self.unpack.data_ptr())
+        for j, ptr in enumerate(self.peer_ptrs):
+            c.peer_dst[j] = int(ptr)
+        return c
+
+
 def _rows_view_ok(t: torch.Tensor, H: int, D: int) -> None:
     if t.dtype != torch.bfloat16:
         raise ValueError("attention operands must be bf16")
@@ -124,8 +151,11 @@ def _rows_view_ok(t: torch.Tensor, H: int, D: int) -> None:
 
 
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSchedule,
-             softmax_scale: float | None = None, out: torch.Tensor | None = None):
-    """Varlen causal attention forward; q/k/v [T, H, D] bf16 (row-strided views OK)."""
+             softmax_scale: float | None = None, out: torch.Tensor | None = None,
+             scatter: HeadScatter | None = None):
+    """Varlen causal attention forward; q/k/v [T, H, D] bf16 (row-strided views OK).
+    `scatter` fuses the head->seq exchange of O into the epilogue (O is still written
+    to `out`)."""
     _require_cuda(q, k, v)
     T, H, D = q.shape
     for t in (q, k, v):
@@ -140,17 +170,22 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
                         q.stride(0), k.stride(0), v.stride(0), o.stride(0),
                         sched.cu_seqlens.data_ptr(), _ptr(sched.seq_starts), sched.fwd_tiles.data_ptr(),
                         sched.n_fwd, sched.n_seq, T, H, D, scale)
+    if scatter is not None:
+        a.scatter = scatter.to_c()
     capi.check(capi.load().fsp_attn_fwd(ctypes.byref(a), _stream()))
     LAUNCHES[0] += 1 if sched.n_fwd else 0
     return o, lse
 
 
 def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | None = None,
-             dq=None, dk=None, dv=None, dq_accum=None, delta=None):
+             dq=None, dk=None, dv=None, dq_accum=None, delta=None,
+             scatter: HeadScatter | None = None):
     """Varlen causal attention backward -> (dq, dk, dv), each [T, H, D] bf16.
 
     dq_accum (fp32 [H, T, D]) and delta (fp32 [H, T]) are optional reusable workspaces
-    (fsp_attn_bwd_workspace_bytes gives their combined size).
+    (fsp_attn_bwd_workspace_bytes gives their combined size).  With `scatter` the
+    head->seq exchange of dQ / dK / dV (destination matrices 0 / 1 / 2) is fused into the
+    kernels and nothing is written locally: the result is (None, None, None).
     """
     _require_cuda(q, k, v, o, dout, lse)
     T, H, D = q.shape
@@ -161,22 +196,30 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
                          f"[{sched.total_rows}, {sched.n_heads}, {sched.head_dim}]")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(D)
     dev = q.device
-    dq = dq if dq is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
-    dk = dk if dk is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
-    dv = dv if dv is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
+    if scatter is None:
+        dq = dq if dq is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
+        dk = dk if dk is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
+        dv = dv if dv is not None else torch.empty((T, H, D), dtype=torch.bfloat16, device=dev)
+    elif dq is not None or dk is not None or dv is not None:
+        raise ValueError("a fused head->seq backward writes no local dq / dk / dv")
     dq_acc = dq_accum if dq_accum is not None else torch.empty((H, T, D), dtype=torch.float32,
                                                                device=dev)
     delta = delta if delta is not None else torch.empty((H, T), dtype=torch.float32, device=dev)
     need = capi.load().fsp_attn_bwd_workspace_bytes(T, H, D)
     if (dq_acc.numel() + delta.numel()) * 4 < need or dq_acc.numel() < T * H * D:
         raise ValueError("attention backward workspace too small")
+    hd = H * D
     a = capi.FspAttnBwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(),
-                        lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                        lse.data_ptr(), _ptr(dq), _ptr(dk), _ptr(dv),
                         q.stride(0), k.stride(0), v.stride(0), o.stride(0), dout.stride(0),
-                        dq.stride(0), dk.stride(0), dv.stride(0), dq_acc.data_ptr(),
+                        dq.stride(0) if dq is not None else hd,
+                        dk.stride(0) if dk is not None else hd,
+                        dv.stride(0) if dv is not None else hd, dq_acc.data_ptr(),
                         delta.data_ptr(), sched.cu_seqlens.data_ptr(), _ptr(sched.seq_starts),
                         sched.bwd_tiles.data_ptr(),
                         sched.n_bwd, sched.n_seq, T, H, D, scale)
+    if scatter is not None:
+        a.scatter = scatter.to_c()
     capi.check(capi.load().fsp_attn_bwd(ctypes.byref(a), _stream()))
     LAUNCHES[0] += (2 if T else 0) + (1 if sched.n_bwd else 0)
     return dq, dk, dv

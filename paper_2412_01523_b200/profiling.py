@@ -53,7 +53,15 @@ class EventTimer:
             d["ms"] += s.elapsed_time(e)
             d["n"] += 1
             d["work"] += work
+        for name, w in self.work.items():  # counters without a device span (count())
+            out.setdefault(name, {"ms": 0.0, "n": 0, "work": 0.0})["work"] += w
         return out
+
+    def count(self, name: str, work: float) -> None:
+        """Accumulate work that has no span of its own (e.g. bytes moved inside a kernel
+        timed under another name)."""
+        if self.enabled:
+            self.work[name] += work
 
 
 # Kernel launches issued by the C-ABI calls made through ops.py (the bench's

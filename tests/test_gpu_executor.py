@@ -92,6 +92,76 @@ def test_a2a_emulated_group_bit_exact(degree, H):
         assert torch.equal(outs[j].cpu(), locals_[j].cpu())
 
 
+@pytest.mark.parametrize("degree,H,D", [(2, 4, 128), (4, 10, 128), (8, 13, 128), (2, 4, 64)])
+def test_fused_head2seq_matches_separate_exchange(degree, H, D):
+    """Eq. (4) fused into the attention epilogues (FspHeadScatter, ABI 4) stores exactly
+    what the attention launch followed by fsp_a2a_head2seq stores: O (forward) and dK / dV
+    (backward) bit for bit, dQ to the fp32 reduction order of its atomics; every member
+    of an emulated group on one GPU, uneven head splits included."""
+    ops = _ops()
+    from paper_2412_01523_b200.layout import build_microbatch_layout, head_split
+    lengths = [333, 1, 128, 77, 1000, 260]
+    mb = {"selected_groups": [{"slot_id": 0, "degree": degree,
+                               "sequence_indices": [2, 0, 4, 1, 3, 5]}]}
+    lay = build_microbatch_layout(mb, lengths, degree, n_heads=H)
+    grp = lay.groups[0]
+    hb = head_split(H, degree)
+    R, T = grp.rows_per_rank, grp.padded_tokens
+    n_loc = [int((grp.shard(j) >= 0).sum()) for j in range(degree)]
+    table = torch.from_numpy(np.ascontiguousarray(grp.unpack_table().reshape(-1))).cuda()
+    g = torch.Generator().manual_seed(7 + degree)
+    ref_o = [torch.zeros(n, H, D, dtype=torch.bfloat16, device="cuda") for n in n_loc]
+    got_o = [torch.zeros_like(t) for t in ref_o]
+    ref_d = [torch.zeros(n, 3, H, D, dtype=torch.bfloat16, device="cuda") for n in n_loc]
+    got_d = [torch.zeros_like(t) for t in ref_d]
+    for j in range(degree):
+        hn = hb[j + 1] - hb[j]
+        sched = ops.AttnSchedule.build(grp.cu_seqlens, "cuda", hn, total_rows=T, head_dim=D)
+        qkv = torch.randn(T, 3, hn, D, generator=g).bfloat16().cuda()
+        dout = torch.randn(T, hn, D, generator=g).bfloat16().cuda()
+        q, k, v = qkv[:, 0], qkv[:, 1], qkv[:, 2]
+        o, lse = ops.attn_fwd(q, k, v, sched)
+        hm = max(b - a for a, b in zip(hb, hb[1:]))  # head slots of the head-sharded side
+        o_pad = torch.zeros(T, hm, D, dtype=torch.bfloat16, device="cuda")
+        o_pad[:, :hn] = o
+        ops.a2a("head2seq", o_pad.view(T, hm * D), [t.data_ptr() for t in ref_o], degree=degree,
+                rank=j, rows_per_rank=R, n_mats=1, n_heads=H, head_dim=D, dst_stride=H * D,
+                index=table, head_begin=hb)
+        sc = ops.HeadScatter(degree, R, hb[j], H * D, 0, table, [t.data_ptr() for t in got_o])
+        o2, _ = ops.attn_fwd(q, k, v, sched, scatter=sc)
+        n_real = int(grp.cu_seqlens[-1])  # rows past it are pad rows nobody writes
+        assert torch.equal(o2[:n_real], o[:n_real])  # the local copy is still written
+        dq, dk, dv = ops.attn_bwd(q, k, v, o, dout, lse, sched)
+        dqkv = torch.zeros(T, 3, hm, D, dtype=torch.bfloat16, device="cuda")
+        dqkv[:, :, :hn] = torch.stack([dq, dk, dv], dim=1)
+        ops.a2a("head2seq", dqkv.view(T, 3 * hm * D), [t.data_ptr() for t in ref_d],
+                degree=degree, rank=j, rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D,
+                dst_stride=3 * H * D, index=table, head_begin=hb)
+        sc = ops.HeadScatter(degree, R, hb[j], 3 * H * D, H * D, table,
+                             [t.data_ptr() for t in got_d])
+        assert ops.attn_bwd(q, k, v, o, dout, lse, sched, scatter=sc) == (None, None, None)
+    torch.cuda.synchronize()
+    for j in range(degree):
+        assert torch.equal(got_o[j], ref_o[j])
+        assert torch.equal(got_d[j][:, 1:], ref_d[j][:, 1:])
+        torch.testing.assert_close(got_d[j][:, 0].float(), ref_d[j][:, 0].float(),
+                                   atol=2e-2, rtol=2e-2)
+
+
+def test_fused_head2seq_rejects_bad_tables():
+    ops = _ops()
+    sched = ops.AttnSchedule.build([0, 256], "cuda", 2, total_rows=256, head_dim=128)
+    q = torch.zeros(256, 2, 128, dtype=torch.bfloat16, device="cuda")
+    table = torch.zeros(256, dtype=torch.int32, device="cuda")
+    dst = torch.zeros(256, 4, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):  # degree * rows_per_rank != total rows
+        ops.attn_fwd(q, q, q, sched, scatter=ops.HeadScatter(2, 100, 0, 512, 0, table[:200],
+                                                             [dst.data_ptr()] * 2))
+    with pytest.raises(ValueError):  # destination row too short for head_offset + heads
+        ops.attn_fwd(q, q, q, sched, scatter=ops.HeadScatter(2, 128, 3, 512, 0, table,
+                                                             [dst.data_ptr()] * 2))
+
+
 def _plan_n1(lengths, split):
     mbs = []
     for idx in split:
