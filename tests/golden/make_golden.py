@@ -58,6 +58,18 @@ B200_ATTN_COEFFS = CostCoefficients(alpha1=5.93e-11, alpha2=2.5e-8, beta1=1e-4, 
 B200_E = 180e9
 
 
+def c2_fitted_coeffs() -> CostCoefficients:
+    """The C2 plans' coefficients: fitted by the reference's fit_coefficients to the B200
+    step itself (scripts/calibrate.py on 4xB200 with the round-1 final kernels and the fused
+    head->seq exchange, profiles/r01_calibration_v2.json).  The hand-set
+    B200_ATTN_COEFFS above predated the final kernels: their alpha1/alpha2 ratio made
+    degree-1 groups of ~1K-token sequences look cheaper than they run."""
+    cal = json.loads((ROOT / "profiles" / "r01_calibration_v2.json").read_text())["coefficients"]
+    return CostCoefficients(alpha1=cal["alpha1"], alpha2=cal["alpha2"], beta1=cal["beta1"],
+                            alpha3=cal["alpha3"], beta2=cal["beta2"],
+                            m_token=cal["m_token"], m_ms=cal["m_ms"])
+
+
 def b200_cluster(n: int) -> ClusterSpec:
     return ClusterSpec(n, 1, 1e15, 7.7e11, B200_E)
 
@@ -106,19 +118,7 @@ def main():
     dump("fig1_flexsp.json", plan_doc(p, fb))
     p = plan_static(fb, FIG1_CLUSTER, FIG1_COEFFS, 32)
     dump("fig1_static32.json", plan_doc(p, fb))
-    # C2 at N = 1, 2, 4, 8
-    cb = c2_batch()
-    for n in (1, 2, 4, 8):
-        cl = b200_cluster(n)
-        p = solve_batch(cb, cl, B200_ATTN_COEFFS, SolveConfig(jobs=8, time_limit=60))
-        dump(f"c2_n{n}_flexsp.json", plan_doc(p, cb, {"coefficients": B200_ATTN_COEFFS.to_json_dict(),
-                                                      "cluster": cl.to_json_dict()}))
-        s = plan_static(cb, cl, B200_ATTN_COEFFS, n)
-        dump(f"c2_n{n}_static.json", plan_doc(s, cb, {"coefficients": B200_ATTN_COEFFS.to_json_dict(),
-                                                      "cluster": cl.to_json_dict()}))
-        print(f"C2 N={n}: flexsp {p.predicted_total_time:.5f}s "
-              f"{[sorted((g.degree for g in mb.selected_groups), reverse=True) for mb in p.micro_batches]}"
-              f" static {s.predicted_total_time:.5f}s")
+    make_c2_plans()
     # random small instances for layout parity
     rng = np.random.default_rng(7)
     for i, n in enumerate((4, 8, 4)):
@@ -146,6 +146,22 @@ def main():
                         o=o.numpy(), lse=lse.numpy(), dq=dq.numpy(), dk=dk.numpy(), dv=dv.numpy())
     for key, (text, t) in meta.items():
         print(key, hashlib.sha256(text.encode()).hexdigest()[:16], round(t, 6))
+
+
+def make_c2_plans(prefix: str = "c2"):
+    """C2 at N = 1, 2, 4, 8 with the B200-fitted coefficients (the bench's plans)."""
+    cb = c2_batch()
+    co = c2_fitted_coeffs()
+    for n in (1, 2, 4, 8):
+        cl = b200_cluster(n)
+        extra = {"coefficients": co.to_json_dict(), "cluster": cl.to_json_dict()}
+        p = solve_batch(cb, cl, co, SolveConfig(jobs=8, time_limit=60))
+        dump(f"{prefix}_n{n}_flexsp.json", plan_doc(p, cb, extra))
+        s = plan_static(cb, cl, co, n)
+        dump(f"{prefix}_n{n}_static.json", plan_doc(s, cb, extra))
+        print(f"C2 N={n}: flexsp {p.predicted_total_time:.5f}s "
+              f"{[sorted((g.degree for g in mb.selected_groups), reverse=True) for mb in p.micro_batches]}"
+              f" static {s.predicted_total_time:.5f}s", flush=True)
 
 
 # ---- C3 / C4 (SURVEY.md §8d): 13B-shape (H=40) and 30B-shape (H=52) attention layers.
@@ -212,7 +228,9 @@ def make_scale_configs():
 
 
 if __name__ == "__main__":
-    if "--scale-configs" in sys.argv:  # C3 / C4 plans only
+    if "--c2" in sys.argv:  # C2 plans only
+        make_c2_plans()
+    elif "--scale-configs" in sys.argv:  # C3 / C4 plans only
         make_scale_configs()
     elif "--full-step" in sys.argv:  # C3 full-step plans only
         make_full_step_plans()
