@@ -16,8 +16,10 @@ B200 design:
   (fsp_a2a_seq2head / fsp_a2a_head2seq read/write rows through the layout tables);
 * groups of one micro-batch run concurrently on disjoint ranks; micro-batches run in
   order (gradient accumulation, PAPER.md:378-380);
-* every exchange ends in a peer-memory flag barrier over the group; a world barrier
-  opens each micro-batch because the rank blocks are regrouped there.
+* every exchange ends in a peer-memory flag barrier over the group, and a group entry
+  barrier opens each micro-batch's forward and backward (its members write into each
+  other's heap regions next); groups never wait on each other and degree-1 groups run
+  without any barrier.
 """
 from __future__ import annotations
 
@@ -237,7 +239,11 @@ class FlexSPExecutor:
 
         Returns (out_local view [n_local, H, D], saved) where saved feeds the backward.
         """
-        self._barrier(range(self.world_size), self._next_epoch(), "world_barrier")  # regroup
+        # Entry barrier over this micro-batch's group only: its members are about to write
+        # into each other's heap regions, so every member must be done (in stream order)
+        # with what the previous micro-batch left there.  Ranks of other groups never touch
+        # these heaps, and a degree-1 group touches none, so groups run decoupled.
+        ep_entry = self._next_epoch()
         grp = mb.group
         if grp is None:
             for _ in range(2):
@@ -257,6 +263,7 @@ class FlexSPExecutor:
                 _, lse = ops.attn_fwd(qkv_local[:, 0], qkv_local[:, 1], qkv_local[:, 2], mb.sched,
                                       self.scale, out=out_local)
             return out_local, (qkv_local, out_local, lse)
+        self._barrier(ranks, ep_entry, "entry_barrier")
         off = sp.offsets
         T = grp.padded_tokens
         recv = self.heap.view(off["qkv_recv"], (T, 3, hm, D), torch.bfloat16)
@@ -299,6 +306,7 @@ class FlexSPExecutor:
 
     def micro_batch_backward(self, sp: StepPlan, mb: RankMicroBatch, saved, dout_local: torch.Tensor):
         """Backward of micro_batch_forward: dout_local [n_local, H, D] -> dqkv_local view."""
+        ep_entry = self._next_epoch()  # group entry barrier, as in the forward
         grp = mb.group
         if grp is None:
             for _ in range(2):
@@ -321,6 +329,7 @@ class FlexSPExecutor:
         d, j, R = grp.degree, mb.j, grp.rows_per_rank
         hn, hm, hb = mb.n_heads_local, mb.heads_stride, mb.head_begin
         ranks = grp.ranks
+        self._barrier(ranks, ep_entry, "entry_barrier")
         off = sp.offsets
         T = grp.padded_tokens
         do_recv = self.heap.view(off["do_recv"], (T, hm, D), torch.bfloat16)
