@@ -37,6 +37,7 @@ struct FwdParams {
   int32_t total_rows;
   int32_t n_heads;
   float scale_log2;
+  int32_t n_tiles;  // schedule entries (the persistent pair kernel walks them)
   ScatterDev sc;  // fused head->seq of O (sc.degree == 0: off)
 };
 
@@ -349,6 +350,71 @@ __device__ unsigned int g_fwd_done;
 #define FSP_FTW(slot, call) call
 #endif
 
+// One schedule entry of the pair kernel: query rows [q0, q0 + 256) of one sequence x head.
+struct PairTile {
+  int head, seq_start, seqlen, q0, n_a, n_b, n_kv;
+  bool has_b;
+};
+
+__device__ __forceinline__ PairTile decode_pair(const FwdParams& p, int w) {
+  PairTile t;
+  const int tile = p.tiles[2 * w];
+  t.head = p.tiles[2 * w + 1];
+  const int seq = tile >> 16;
+  const int pair = tile & 0xFFFF;
+  t.seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
+  t.seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
+  t.q0 = pair * 256;
+  t.has_b = t.q0 + 128 < t.seqlen;
+  t.n_a = 2 * pair + 1;                   // kv tiles seen by tile A (causal)
+  t.n_b = t.has_b ? 2 * pair + 2 : 0;     // ... by tile B
+  t.n_kv = t.has_b ? t.n_b : t.n_a;
+  return t;
+}
+
+// Dynamic schedule of the persistent pair kernel: the TMA producer claims the next entry of
+// the longest-first schedule with an atomic on a per-device counter (zeroed by the host before
+// each launch) and hands it to the MMA and softmax warps through a two-slot ring in shared
+// memory — the persistent version of the hardware's "next CTA to the first free SM".
+__device__ int g_fwd_pair_next;
+
+struct EntryRing {
+  int* idx;         // [2] claimed schedule entries
+  uint64_t* full;   // [2] producer -> consumers
+  uint64_t* empty;  // [2] consumers (MMA thread + 8 softmax warps) -> producer
+};
+constexpr int kRingConsumers = 9;
+
+// Producer side: the k-th entry of this CTA (first: blockIdx.x; then claimed dynamically).
+template <bool kPersistent>
+__device__ __forceinline__ int claim_entry(const EntryRing& r, int k) {
+  if (!kPersistent) return k == 0 ? (int)blockIdx.x : INT_MAX;
+  const int slot = k & 1;
+  mbar_wait(r.empty + slot, ((k >> 1) & 1) ^ 1);
+  const int w = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(&g_fwd_pair_next, 1);
+  r.idx[slot] = w;
+  mbar_arrive(r.full + slot);
+  return w;
+}
+
+// Consumer side: either every lane of a softmax warp (kWarp: lane 0 releases the slot
+// after the warp has read it) or the single elected MMA-issuer thread.
+template <bool kPersistent, bool kWarp>
+__device__ __forceinline__ int take_entry(const EntryRing& r, int k) {
+  if (!kPersistent) return k == 0 ? (int)blockIdx.x : INT_MAX;
+  const int slot = k & 1;
+  mbar_wait(r.full + slot, (k >> 1) & 1);
+  const int w = r.idx[slot];
+  if (kWarp) {
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(r.empty + slot);
+  } else {
+    mbar_arrive(r.empty + slot);
+  }
+  return w;
+}
+
+template <bool kPersistent>
 __global__ void __launch_bounds__(kF2Threads, 1)
     attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -366,23 +432,21 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   uint64_t* s_full = bars + 11;  // [2] per tile
   uint64_t* o_done = bars + 13;  // [2] per tile
   uint64_t* p_half = bars + 15;  // [2 tiles][2 halves]: P columns for kv rows 0-63 / 64-127
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+  uint64_t* q_empty = bars + 19; // Q_A / Q_B read by the last QK^T of a schedule entry
+  const EntryRing ring{reinterpret_cast<int*>(bars + 24), bars + 20, bars + 22};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int tile = p.tiles[2 * blockIdx.x];
-  const int head = p.tiles[2 * blockIdx.x + 1];
-  const int seq = tile >> 16;
-  const int pair = tile & 0xFFFF;
-  const int seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
-  const int seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
-  const int q0 = pair * 256;
-  const bool has_b = q0 + 128 < seqlen;
-  const int n_a = 2 * pair + 1;                 // kv tiles seen by tile A (causal)
-  const int n_b = has_b ? 2 * pair + 2 : 0;     // ... by tile B
-  const int n_kv = has_b ? n_b : n_a;
+  // Barrier phases run on across the schedule entries of a persistent CTA: every counter
+  // below is a running count of completions, so a wait's parity is (count & 1).
 
   if (threadIdx.x == 0) {
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(ring.full + i, 1);
+      mbar_init(ring.empty + i, kRingConsumers);
+    }
     mbar_init(bar_q, 1);
     for (int i = 0; i < L::kKStages; ++i) {
       mbar_init(k_full + i, 1);
@@ -410,30 +474,41 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
       tma_prefetch(&tm_v);
-      mbar_expect_tx(bar_q, (has_b ? 2 : 1) * L::kTileBytes);
-      for (int b = 0; b < 2; ++b) {
-        tma_load_3d(smem + L::kQA + b * 16384, &tm_q, bar_q, b * 64, head, seq_start + q0);
-        if (has_b)
-          tma_load_3d(smem + L::kQB + b * 16384, &tm_q, bar_q, b * 64, head, seq_start + q0 + 128);
-      }
-      // issue order K_0, K_1, V_0, K_2, V_1, ...: K is consumed one step before V
-      auto load_k = [&](int j) {
-        const int st = j % L::kKStages;
-        mbar_wait(k_empty + st, ((j / L::kKStages) & 1) ^ 1);
-        mbar_expect_tx(k_full + st, L::kTileBytes);
-        for (int b = 0; b < 2; ++b)
-          tma_load_3d(smem + L::kK + st * L::kTileBytes + b * 16384, &tm_k, k_full + st, b * 64,
-                      head, seq_start + j * 128);
-      };
-      load_k(0);
-      for (int j = 0; j < n_kv; ++j) {
-        if (j + 1 < n_kv) load_k(j + 1);
-        const int st = j & 1;
-        mbar_wait(v_empty + st, ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(v_full + st, L::kTileBytes);
-        for (int b = 0; b < 2; ++b)
-          tma_load_3d(smem + L::kV + st * L::kTileBytes + b * 16384, &tm_v, v_full + st, b * 64,
-                      head, seq_start + j * 128);
+      uint32_t g0 = 0;  // K/V ring position: kv steps issued by this CTA so far
+      for (int k = 0;; ++k) {
+        const int w = claim_entry<kPersistent>(ring, k);
+        if (w >= p.n_tiles) break;
+        const PairTile T = decode_pair(p, w);
+        if (k > 0) mbar_wait(q_empty, (k - 1) & 1);  // previous entry's QK^T MMAs are done
+        mbar_expect_tx(bar_q, (T.has_b ? 2 : 1) * L::kTileBytes);
+        for (int b = 0; b < 2; ++b) {
+          tma_load_3d(smem + L::kQA + b * 16384, &tm_q, bar_q, b * 64, T.head, T.seq_start + T.q0);
+          if (T.has_b)
+            tma_load_3d(smem + L::kQB + b * 16384, &tm_q, bar_q, b * 64, T.head,
+                        T.seq_start + T.q0 + 128);
+        }
+        // issue order K_0, K_1, V_0, K_2, V_1, ...: K is consumed one step before V
+        auto load_k = [&](int j) {
+          const uint32_t g = g0 + j;
+          const int st = g % L::kKStages;
+          mbar_wait(k_empty + st, ((g / L::kKStages) & 1) ^ 1);
+          mbar_expect_tx(k_full + st, L::kTileBytes);
+          for (int b = 0; b < 2; ++b)
+            tma_load_3d(smem + L::kK + st * L::kTileBytes + b * 16384, &tm_k, k_full + st, b * 64,
+                        T.head, T.seq_start + j * 128);
+        };
+        load_k(0);
+        for (int j = 0; j < T.n_kv; ++j) {
+          if (j + 1 < T.n_kv) load_k(j + 1);
+          const uint32_t g = g0 + j;
+          const int st = g & 1;
+          mbar_wait(v_empty + st, ((g >> 1) & 1) ^ 1);
+          mbar_expect_tx(v_full + st, L::kTileBytes);
+          for (int b = 0; b < 2; ++b)
+            tma_load_3d(smem + L::kV + st * L::kTileBytes + b * 16384, &tm_v, v_full + st, b * 64,
+                        T.head, T.seq_start + j * 128);
+        }
+        g0 += T.n_kv;
       }
     }
     __syncwarp();
@@ -449,68 +524,85 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       const long long t_start = clock64();
 #endif
-      FSP_FTW(5, mbar_wait(bar_q, 0));
-      auto qk = [&](int x, int j) {  // S_x = Q_x K_j^T
-        const uint32_t qbase = x ? qb : qa;
-        const uint32_t kb = k_base + (j % L::kKStages) * L::kTileBytes;
+      uint32_t g0 = 0;                 // K/V ring position (kv steps consumed so far)
+      uint32_t p_cnt[2] = {0u, 0u};    // p_half completions consumed per tile x
+      int steps = 0;
+      for (int k = 0;; ++k) {
+        const int w = take_entry<kPersistent, false>(ring, k);
+        if (w >= p.n_tiles) break;
+        const PairTile T = decode_pair(p, w);
+        const int n_a = T.n_a, n_b = T.n_b, n_kv = T.n_kv;
+        int qk_left = n_a + n_b;  // QK^T groups still to issue; the last one frees Q_A / Q_B
+        FSP_FTW(5, mbar_wait(bar_q, k & 1));
+        auto qk = [&](int x, int j) {  // S_x = Q_x K_j^T
+          const uint32_t qbase = x ? qb : qa;
+          const uint32_t kb = k_base + ((g0 + j) % L::kKStages) * L::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma_ss(tmem + x * 128, make_sdesc_sw128(qbase + off, 16, 1024),
-                 make_sdesc_sw128(kb + off, 16, 1024), idesc_s, kk > 0);
-        }
-        tc_commit(s_full + x);
-      };
-      auto pv = [&](int x, int j) {  // O_x += P_x V_j, each half as soon as its P lands
-        const uint32_t vb = v_base + (j & 1) * L::kTileBytes;
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma_ss(tmem + x * 128, make_sdesc_sw128(qbase + off, 16, 1024),
+                   make_sdesc_sw128(kb + off, 16, 1024), idesc_s, kk > 0);
+          }
+          tc_commit(s_full + x);
+          if (--qk_left == 0) tc_commit(q_empty);
+        };
+        auto pv = [&](int x, int j) {  // O_x += P_x V_j, each half as soon as its P lands
+          const uint32_t vb = v_base + ((g0 + j) & 1) * L::kTileBytes;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          FSP_FTW(x, mbar_wait(p_half + 2 * x + hh, j & 1));
+          for (int hh = 0; hh < 2; ++hh) {
+            FSP_FTW(x, mbar_wait(p_half + 2 * x + hh, (p_cnt[x] + j) & 1));
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
+              mma_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8,
+                     make_sdesc_sw128(vb + kk * 2048, 16384, 1024), idesc_o,
+                     (j > 0 || kk > 0) ? 1u : 0u);
+          }
+        };
+        auto wait_k = [&](int j) {
+          const uint32_t g = g0 + j;
+          FSP_FTW(2, mbar_wait(k_full + g % L::kKStages, (g / L::kKStages) & 1));
           tc_fence_after();
-#pragma unroll
-          for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
-            mma_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8,
-                   make_sdesc_sw128(vb + kk * 2048, 16384, 1024), idesc_o,
-                   (j > 0 || kk > 0) ? 1u : 0u);
-        }
-      };
-      auto wait_k = [&](int j) {
-        FSP_FTW(2, mbar_wait(k_full + j % L::kKStages, (j / L::kKStages) & 1));
-        tc_fence_after();
-      };
-      wait_k(0);
-      qk(0, 0);
-      if (n_b > 0) qk(1, 0);
-      tc_commit(k_empty + 0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        const bool next = j + 1 < n_kv;
-        FSP_FTW(3, mbar_wait(v_full + st, (j >> 1) & 1));
-        if (j < n_a) {
-          pv(0, j);
-          if (j + 1 < n_a) {
-            wait_k(j + 1);
-            qk(0, j + 1);
-          } else {
-            tc_commit(o_done + 0);
+        };
+        wait_k(0);
+        qk(0, 0);
+        if (n_b > 0) qk(1, 0);
+        tc_commit(k_empty + g0 % L::kKStages);
+        for (int j = 0; j < n_kv; ++j) {
+          const uint32_t g = g0 + j;
+          const int st = g & 1;
+          const bool next = j + 1 < n_kv;
+          FSP_FTW(3, mbar_wait(v_full + st, (g >> 1) & 1));
+          if (j < n_a) {
+            pv(0, j);
+            if (j + 1 < n_a) {
+              wait_k(j + 1);
+              qk(0, j + 1);
+            } else {
+              tc_commit(o_done + 0);
+            }
           }
-        }
-        if (j < n_b) {
-          pv(1, j);
-          if (j + 1 < n_b) {
-            wait_k(j + 1);
-            qk(1, j + 1);
-          } else {
-            tc_commit(o_done + 1);
+          if (j < n_b) {
+            pv(1, j);
+            if (j + 1 < n_b) {
+              wait_k(j + 1);
+              qk(1, j + 1);
+            } else {
+              tc_commit(o_done + 1);
+            }
           }
+          tc_commit(v_empty + st);
+          if (next) tc_commit(k_empty + (g + 1) % L::kKStages);
         }
-        tc_commit(v_empty + st);
-        if (next) tc_commit(k_empty + (j + 1) % L::kKStages);
+        p_cnt[0] += n_a;
+        p_cnt[1] += n_b;
+        g0 += n_kv;
+        steps += n_a + n_b;
       }
 #if FSP_FWD_TIMING
       tw[7] = clock64() - t_start;
       for (int i = 0; i < 8; ++i) atomicAdd(&g_fwd_wait[i], (unsigned long long)tw[i]);
-      atomicAdd(&g_fwd_wait[8], (unsigned long long)(n_a + n_b));
+      atomicAdd(&g_fwd_wait[8], (unsigned long long)steps);
       __threadfence();
       if (atomicAdd(&g_fwd_done, 1u) == gridDim.x - 1) {
         printf("fwd MMA issuer cycles (sum over CTAs): tile-steps %llu total %llu | p_half A %llu "
@@ -532,16 +624,23 @@ __global__ void __launch_bounds__(kF2Threads, 1)
     const int row = quad * 32 + lane;
     const uint32_t lane_addr = (quad * 32u) << 16;
     const uint32_t s_col = x * 128, o_col = 256 + x * 128;
-    const int q_pos = q0 + x * 128 + row;
-    const int n_x = x ? n_b : n_a;
     const float sl2 = p.scale_log2;
+    uint32_t s_cnt = 0, o_cnt = 0;  // s_full / o_done completions this tile x consumed
+    for (int k = 0;; ++k) {
+    const int w = take_entry<kPersistent, true>(ring, k);
+    if (w >= p.n_tiles) break;
+    const PairTile T = decode_pair(p, w);
+    const int head = T.head, seq_start = T.seq_start, seqlen = T.seqlen, q0 = T.q0;
+    const int n_x = x ? T.n_b : T.n_a;
+    if (n_x == 0) continue;  // no tile B in this entry
+    const int q_pos = q0 + x * 128 + row;
     float m = -INFINITY;  // exponent base (scaled, log2 units)
     float l = 0.f;
     for (int j = 0; j < n_x; ++j) {
 #if FSP_FWD_TIMING
       const long long ts0 = clock64();
 #endif
-      mbar_wait(s_full + x, j & 1);
+      mbar_wait(s_full + x, (s_cnt + j) & 1);
 #if FSP_FWD_TIMING
       const long long ts1 = clock64();
       if (warp == 2 && lane == 0) atomicAdd(&g_fwd_wait[9], (unsigned long long)(ts1 - ts0));
@@ -713,13 +812,17 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       if (warp == 2 && lane == 0) atomicAdd(&g_fwd_wait[10], (unsigned long long)(clock64() - ts1));
 #endif
     }
+    s_cnt += n_x;
     // ------------------------------------------------------------ epilogue
-    if (n_x > 0) {
-      mbar_wait(o_done + x, 0);
+    {
+      mbar_wait(o_done + x, o_cnt & 1);
+      ++o_cnt;
       tc_fence_after();
       const float inv_l = 1.f / l;
       const bool valid = q_pos < seqlen;
-      if (p.sc.degree) {
+      // (the staged path borrows this entry's Q buffer, which a persistent CTA refills for
+      // its next entry: the host never combines the fused exchange with the persistent launch)
+      if (!kPersistent && p.sc.degree) {
         // Fused head->seq (Eq. 4): O goes to its owner's sequence shard over NVLink as well
         // as to the local buffer.  One-row-per-thread 16-byte stores would cross NVLink as
         // 32 scattered 16-byte packets per warp instruction, so the warp first stages its
@@ -781,6 +884,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         p.lse[(int64_t)head * p.total_rows + seq_start + q_pos] =
             (m + __log2f(l)) * 0.69314718055994531f;
     }
+    }  // schedule entries
   }
   tc_fence_before();
   __syncthreads();
@@ -817,11 +921,29 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   p.n_heads = a->n_heads;
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
   if ((rc = scatter_from_abi(a->scatter, 1, a->n_heads, D, a->total_rows, &p.sc))) return rc;
+  p.n_tiles = a->n_tiles;
   if (D == 128) {  // schedule entries are 256-row tile pairs (fsp_attn_schedule, head_dim 128)
     const int smem = Fwd2Smem::kBytes + 1024;
-    FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
-    attn_fwd_pair_kernel<<<(unsigned)a->n_tiles, kF2Threads, smem, stream>>>(tq, tk, tv, p);
+    // Persistent launch (one CTA per SM walking the schedule, so an entry's Q load and first
+    // QK^T overlap the previous entry's softmax tail and epilogue) unless the head->seq
+    // exchange is fused, whose epilogue stages rows in the entry's Q buffer.
+    int sms = 0, dev = 0;
+    FSP_CUDA(cudaGetDevice(&dev));
+    FSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const char* env = getenv("FSP_FWD_PERSISTENT");
+    const bool persistent = p.sc.degree == 0 && !(env && env[0] == '0') && a->n_tiles > sms;
+    if (persistent) {
+      void* ctr = nullptr;
+      FSP_CUDA(cudaGetSymbolAddress(&ctr, g_fwd_pair_next));
+      FSP_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), stream));
+      FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attn_fwd_pair_kernel<true><<<(unsigned)sms, kF2Threads, smem, stream>>>(tq, tk, tv, p);
+    } else {
+      FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attn_fwd_pair_kernel<false><<<(unsigned)a->n_tiles, kF2Threads, smem, stream>>>(tq, tk, tv, p);
+    }
   } else {
     const int smem = FwdSmem<D>::kBytes + 1024;
     FSP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -106,3 +106,33 @@ def test_attn_bwd_matches_oracle(lengths, H, D):
         torch.testing.assert_close(got, ref, atol=5e-2, rtol=5e-2)
         if ref.abs().max() > 0:
             assert _cos(got, ref) >= 0.999
+
+
+@pytest.mark.parametrize("lengths,H", [
+    ([20000, 1, 129, 3000, 256, 2048] + [1024] * 40, 4),   # long + many short sequences
+    ([300] * 600, 2),                                       # many one-pair entries
+])
+def test_fwd_persistent_matches_classic(lengths, H, monkeypatch):
+    """The persistent pair-kernel launch (one CTA per SM claiming schedule entries
+    dynamically; used when the schedule has more entries than SMs) computes exactly what
+    the one-CTA-per-entry launch computes: O and LSE bit for bit."""
+    from paper_2412_01523_b200 import ops
+    cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32)
+    T = int(cu[-1])
+    g = torch.Generator().manual_seed(99)
+    qkv = torch.randn(T, 3, H, 128, generator=g).bfloat16().cuda()
+    sched = ops.AttnSchedule.build(cu, "cuda", H, head_dim=128)
+    assert sched.n_fwd > torch.cuda.get_device_properties(0).multi_processor_count
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("FSP_FWD_PERSISTENT", mode)
+        o, lse = ops.attn_fwd(qkv[:, 0], qkv[:, 1], qkv[:, 2], sched)
+        torch.cuda.synchronize()
+        outs[mode] = (o.clone(), lse.clone())
+    assert torch.equal(outs["0"][0], outs["1"][0])
+    assert torch.equal(outs["0"][1], outs["1"][1])
+    # and the persistent result against the fp32 oracle on a few sequences
+    a, b = int(cu[1]), int(cu[4])  # sequences 1..3
+    sub = qkv[a:b].cpu()
+    o_ref, _ = attention_fwd_ref(sub[:, 0], sub[:, 1], sub[:, 2], (cu[1:5] - cu[1]).astype(np.int32))
+    assert (outs["1"][0][a:b].float().cpu() - o_ref).abs().max() <= 2e-2
