@@ -51,6 +51,7 @@ struct BwdParams {
   int32_t n_heads;
   float scale;
   float scale_log2;
+  int32_t n_tiles;  // schedule entries (the persistent kernel walks them)
   ScatterDev sc;  // fused head->seq of dK / dV (matrices 1, 2); sc.degree == 0: off
 };
 
@@ -467,6 +468,69 @@ __device__ unsigned int g_bwd_done;
 #define FSP_TW(slot, call) call
 #endif
 
+// One schedule entry of the backward: 128 kv rows (kv tile kt) of one sequence x head.
+struct KvTile {
+  int head, seq_start, seqlen, kt, kv0, nq, n_it, n_u;
+};
+
+__device__ __forceinline__ KvTile decode_kv(const BwdParams& p, int w) {
+  KvTile t;
+  const int tile = p.tiles[2 * w];
+  t.head = p.tiles[2 * w + 1];
+  const int seq = tile >> 16;
+  t.kt = tile & 0xFFFF;
+  t.seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
+  t.seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
+  t.kv0 = t.kt * kTile;
+  t.nq = (t.seqlen + kTile - 1) / kTile;
+  t.n_it = t.nq - t.kt;
+  t.n_u = 2 * t.n_it;
+  return t;
+}
+
+// Dynamic schedule of the persistent launch (as in the forward): the TMA producer claims
+// entries with an atomic on a per-device counter zeroed by the host before the launch and
+// hands them to the other roles through a two-slot shared-memory ring.
+__device__ int g_bwd_next;
+
+struct BwdEntryRing {
+  int* idx;
+  uint64_t* full;
+  uint64_t* empty;
+};
+constexpr int kBwdRingConsumers = 1 + kV2Compute + kV2Reduce;  // MMA thread + warps
+
+template <bool kPersistent>
+__device__ __forceinline__ int bwd_claim(const BwdEntryRing& r, int k) {
+  if (!kPersistent) return k == 0 ? (int)blockIdx.x : INT_MAX;
+  const int slot = k & 1;
+  mbar_wait(r.empty + slot, ((k >> 1) & 1) ^ 1);
+  const int w = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(&g_bwd_next, 1);
+  r.idx[slot] = w;
+  mbar_arrive(r.full + slot);
+  return w;
+}
+
+template <bool kPersistent, bool kWarp>
+__device__ __forceinline__ int bwd_take(const BwdEntryRing& r, int k) {
+  if (!kPersistent) return k == 0 ? (int)blockIdx.x : INT_MAX;
+  const int slot = k & 1;
+  mbar_wait(r.full + slot, (k >> 1) & 1);
+  const int w = r.idx[slot];
+  if (kWarp) {
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(r.empty + slot);
+  } else {
+    mbar_arrive(r.empty + slot);
+  }
+  return w;
+}
+
+// kPersistent: one CTA per SM walks the schedule (dynamic claims); the next entry's K/V load
+// and first S^T/dP^T MMAs overlap this entry's dK/dV epilogue.  Barrier phases and the
+// Q/dO ring run on across entries: every parity below derives from running counts (global
+// unit index U, global query-tile index IT = U / 2, entry count k).
+template <bool kPersistent>
 __global__ void __launch_bounds__(kV2Threads, 1)
     attn_bwd_kernel_v2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
@@ -480,7 +544,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* bar_kv = bars + 0;
   constexpr int kR = L::kSlots;
-  static_assert(1 + 2 * kR + 9 <= 32, "barrier region holds 32 mbarriers");
+  static_assert(1 + 2 * kR + 15 <= 32, "barrier region holds 32 mbarriers");
   uint64_t* ring_full = bars + 1;            // [kSlots]
   uint64_t* ring_empty = bars + 1 + kR;      // [kSlots]
   uint64_t* s_full = bars + 1 + 2 * kR;      // [2]
@@ -488,20 +552,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   uint64_t* dq_full = s_full + 4;            // [2]
   uint64_t* tm_free = s_full + 6;            // [2]
   uint64_t* acc_done = s_full + 8;           // dK / dV final
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 9);
+  const BwdEntryRing ering{reinterpret_cast<int*>(s_full + 13), s_full + 9, s_full + 11};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 14);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int tile = p.tiles[2 * blockIdx.x];
-  const int head = p.tiles[2 * blockIdx.x + 1];
-  const int seq = tile >> 16;
-  const int kt = tile & 0xFFFF;
-  const int seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
-  const int seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
-  const int kv0 = kt * kTile;
-  const int nq = (seqlen + kTile - 1) / kTile;
-  const int n_it = nq - kt;
-  const int n_u = 2 * n_it;
 
   if (threadIdx.x == 0) {
     mbar_init(bar_kv, 1);
@@ -514,6 +569,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       mbar_init(p_ready + i, kV2Compute);
       mbar_init(dq_full + i, 1);
       mbar_init(tm_free + i, kV2Reduce);
+      mbar_init(ering.full + i, 1);
+      mbar_init(ering.empty + i, kBwdRingConsumers);
     }
     mbar_init(acc_done, 1);
     fence_mbar_init();
@@ -531,22 +588,31 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       tma_prefetch(&tm_k);
       tma_prefetch(&tm_v);
       tma_prefetch(&tm_do);
-      mbar_expect_tx(bar_kv, 2 * L::kTileBytes);
-      for (int b = 0; b < 2; ++b) {
-        tma_load_3d(smem + L::kK + b * 16384, &tm_k, bar_kv, b * 64, head, seq_start + kv0);
-        tma_load_3d(smem + L::kV + b * 16384, &tm_v, bar_kv, b * 64, head, seq_start + kv0);
-      }
-      // items 2u / 2u+1 = Q / dO rows of half tile u (64 rows each)
-      for (int item = 0; item < 2 * n_u; ++item) {
-        const int slot = item % L::kSlots;
-        const uint32_t ph = (item / L::kSlots) & 1;
-        const int row = seq_start + kv0 + (item >> 1) * 64;
-        mbar_wait(ring_empty + slot, ph ^ 1);
-        mbar_expect_tx(ring_full + slot, L::kHalfBytes);
-        const CUtensorMap* map = (item & 1) ? &tm_do : &tm_q;
-        for (int b = 0; b < 2; ++b)
-          tma_load_3d(smem + L::kRing + slot * L::kHalfBytes + b * 8192, map, ring_full + slot,
-                      b * 64, head, row);
+      uint32_t U0 = 0;  // global index of the entry's first 64-query unit
+      for (int k = 0;; ++k) {
+        const int w = bwd_claim<kPersistent>(ering, k);
+        if (w >= p.n_tiles) break;
+        const KvTile T = decode_kv(p, w);
+        if (k > 0) mbar_wait(acc_done, (k - 1) & 1);  // the previous entry's MMAs read K / V
+        mbar_expect_tx(bar_kv, 2 * L::kTileBytes);
+        for (int b = 0; b < 2; ++b) {
+          tma_load_3d(smem + L::kK + b * 16384, &tm_k, bar_kv, b * 64, T.head, T.seq_start + T.kv0);
+          tma_load_3d(smem + L::kV + b * 16384, &tm_v, bar_kv, b * 64, T.head, T.seq_start + T.kv0);
+        }
+        // items 2U / 2U+1 = Q / dO rows of half tile U (64 rows each)
+        for (int li = 0; li < 2 * T.n_u; ++li) {
+          const uint32_t item = 2 * U0 + li;
+          const int slot = item % L::kSlots;
+          const uint32_t ph = (item / L::kSlots) & 1;
+          const int row = T.seq_start + T.kv0 + (li >> 1) * 64;
+          mbar_wait(ring_empty + slot, ph ^ 1);
+          mbar_expect_tx(ring_full + slot, L::kHalfBytes);
+          const CUtensorMap* map = (li & 1) ? &tm_do : &tm_q;
+          for (int b = 0; b < 2; ++b)
+            tma_load_3d(smem + L::kRing + slot * L::kHalfBytes + b * 8192, map, ring_full + slot,
+                        b * 64, T.head, row);
+        }
+        U0 += T.n_u;
       }
     }
     __syncwarp();
@@ -566,86 +632,98 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       const long long t_start = clock64();
 #endif
-      FSP_TW(6, mbar_wait(bar_kv, 0));
-      auto grads = [&](int u) {
-        const int it = u >> 1, h = u & 1;
-        const int sq = (2 * u) % L::kSlots, sd = (2 * u + 1) % L::kSlots;
-        const uint32_t q_base = ring_base + sq * L::kHalfBytes;
-        const uint32_t do_base = ring_base + sd * L::kHalfBytes;
-        const uint32_t dsb = ds_base + h * 16384;
-        FSP_TW(3, mbar_wait(p_ready + h, it & 1));
+      uint32_t U0 = 0;  // global unit index of the entry's first unit
+      int units = 0;
+      for (int k = 0;; ++k) {
+        const int w = bwd_take<kPersistent, false>(ering, k);
+        if (w >= p.n_tiles) break;
+        const int n_u = decode_kv(p, w).n_u;
+        FSP_TW(6, mbar_wait(bar_kv, k & 1));
         tc_fence_after();
-        // dQ^T first and committed on its own, so the reduction warps drain it while dV and
-        // dK (and the next S^T) keep the tensor core busy: dP^T(u+2) waits on that drain.
-        if (u >= 2) FSP_TW(4, mbar_wait(tm_free + h, ((u >> 1) - 1) & 1));  // dQ^T(u-2) drained
-        tc_fence_after();
+        auto grads = [&](int u) {
+          const uint32_t U = U0 + u, IT = U >> 1;
+          const int h = U & 1;
+          const int sq = (2 * U) % L::kSlots, sd = (2 * U + 1) % L::kSlots;
+          const uint32_t q_base = ring_base + sq * L::kHalfBytes;
+          const uint32_t do_base = ring_base + sd * L::kHalfBytes;
+          const uint32_t dsb = ds_base + h * 16384;
+          FSP_TW(3, mbar_wait(p_ready + h, IT & 1));
+          tc_fence_after();
+          // dQ^T first and committed on its own, so the reduction warps drain it while dV and
+          // dK (and the next S^T) keep the tensor core busy: dP^T(U+2) waits on that drain.
+          if (U >= 2) FSP_TW(4, mbar_wait(tm_free + h, (IT - 1) & 1));  // dQ^T(U-2) drained
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 kv rows)
-          if (!(FSP_BWD_ABLATE & 4))
-          mma_ss(tmem + kV2ColDP + h * 64, make_sdesc_sw128(k_base + kk * 2048, 16384, 1024),
-                 make_sdesc_sw128(dsb + kk * 2048, 16384, 1024), idesc_dqt, kk > 0);
-        tc_commit(dq_full + h);
+          for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 kv rows)
+            if (!(FSP_BWD_ABLATE & 4))
+            mma_ss(tmem + kV2ColDP + h * 64, make_sdesc_sw128(k_base + kk * 2048, 16384, 1024),
+                   make_sdesc_sw128(dsb + kk * 2048, 16384, 1024), idesc_dqt, kk > 0);
+          tc_commit(dq_full + h);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO_h      (K = 64 query rows)
-          // P^T of query columns [16kk, 16kk+16): compute warp ch wrote its kV2Cols columns
-          // as bf16 pairs into the first half of its own S columns [ch*kV2Cols, ...) — S
-          // columns it read itself, so no cross-warp barrier is needed
-          mma_ts(tmem + kColDV,
-                 tmem + kV2ColS + h * 64 + (16 * kk / kV2Cols) * kV2Cols + (16 * kk % kV2Cols) / 2,
-                 make_sdesc_sw128(do_base + kk * 2048, 8192, 1024), idesc_dvdk,
-                 (u > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // dK += dS^T Q_h
-          if (FSP_BWD_ABLATE & 8) continue;
-          if (FSP_BWD_DS_TMEM)  // TS: dS^T from the second half of the writer warp's S columns
-            mma_ts(tmem + kColDK,
-                   tmem + kV2ColS + h * 64 + (16 * kk / kV2Cols) * kV2Cols + (16 * kk % kV2Cols) / 2 +
-                       kV2Cols / 2,
-                   make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
+          for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO_h      (K = 64 query rows)
+            // P^T of query columns [16kk, 16kk+16): compute warp ch wrote its kV2Cols columns
+            // as bf16 pairs into the first half of its own S columns [ch*kV2Cols, ...) — S
+            // columns it read itself, so no cross-warp barrier is needed
+            mma_ts(tmem + kColDV,
+                   tmem + kV2ColS + h * 64 + (16 * kk / kV2Cols) * kV2Cols + (16 * kk % kV2Cols) / 2,
+                   make_sdesc_sw128(do_base + kk * 2048, 8192, 1024), idesc_dvdk,
                    (u > 0 || kk > 0) ? 1u : 0u);
-          else
-            mma_ss(tmem + kColDK, make_sdesc_sw128(dsb + kk * 32, 16, 1024),
-                   make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
-                   (u > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc_commit(ring_empty + sq);
-        tc_commit(ring_empty + sd);
-        if (u == n_u - 1) tc_commit(acc_done);
-      };
-      for (int u = 0; u < n_u; ++u) {
-        const int h = u & 1;
-        const int sq = (2 * u) % L::kSlots, sd = (2 * u + 1) % L::kSlots;
-        const uint32_t q_base = ring_base + sq * L::kHalfBytes;
-        const uint32_t do_base = ring_base + sd * L::kHalfBytes;
-        // S^T(u) overwrites P^T(u-2), read by dV of grads(u-2) (issued earlier, in order);
-        // dP^T(u) overwrites dQ^T(u-2): wait until the reduction warps drained it.
-        FSP_TW(0, mbar_wait(ring_full + sq, ((2 * u) / L::kSlots) & 1));
-        tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          mma_ss(tmem + kV2ColS + h * 64,
-                 make_sdesc_sw128(k_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                 make_sdesc_sw128(q_base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_s,
-                 kk > 0);
-        }
-        if (u >= 2) FSP_TW(1, mbar_wait(tm_free + h, ((u >> 1) - 1) & 1));
-        FSP_TW(2, mbar_wait(ring_full + sd, ((2 * u + 1) / L::kSlots) & 1));
-        tc_fence_after();
+          for (int kk = 0; kk < 4; ++kk) {  // dK += dS^T Q_h
+            if (FSP_BWD_ABLATE & 8) continue;
+            if (FSP_BWD_DS_TMEM)  // TS: dS^T from the second half of the writer warp's S columns
+              mma_ts(tmem + kColDK,
+                     tmem + kV2ColS + h * 64 + (16 * kk / kV2Cols) * kV2Cols + (16 * kk % kV2Cols) / 2 +
+                         kV2Cols / 2,
+                     make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
+                     (u > 0 || kk > 0) ? 1u : 0u);
+            else
+              mma_ss(tmem + kColDK, make_sdesc_sw128(dsb + kk * 32, 16, 1024),
+                     make_sdesc_sw128(q_base + kk * 2048, 8192, 1024), idesc_dvdk,
+                     (u > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(ring_empty + sq);
+          tc_commit(ring_empty + sd);
+          if (u == n_u - 1) tc_commit(acc_done);
+        };
+        for (int u = 0; u < n_u; ++u) {
+          const uint32_t U = U0 + u, IT = U >> 1;
+          const int h = U & 1;
+          const int sq = (2 * U) % L::kSlots, sd = (2 * U + 1) % L::kSlots;
+          const uint32_t q_base = ring_base + sq * L::kHalfBytes;
+          const uint32_t do_base = ring_base + sd * L::kHalfBytes;
+          // S^T(U) overwrites P^T(U-2), read by dV of grads(U-2) (issued earlier, in order);
+          // dP^T(U) overwrites dQ^T(U-2): wait until the reduction warps drained it.
+          FSP_TW(0, mbar_wait(ring_full + sq, ((2 * U) / L::kSlots) & 1));
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          mma_ss(tmem + kV2ColDP + h * 64,
-                 make_sdesc_sw128(v_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                 make_sdesc_sw128(do_base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_s,
-                 kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            mma_ss(tmem + kV2ColS + h * 64,
+                   make_sdesc_sw128(k_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                   make_sdesc_sw128(q_base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_s,
+                   kk > 0);
+          }
+          if (U >= 2) FSP_TW(1, mbar_wait(tm_free + h, (IT - 1) & 1));
+          FSP_TW(2, mbar_wait(ring_full + sd, ((2 * U + 1) / L::kSlots) & 1));
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            mma_ss(tmem + kV2ColDP + h * 64,
+                   make_sdesc_sw128(v_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                   make_sdesc_sw128(do_base + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_s,
+                   kk > 0);
+          }
+          tc_commit(s_full + h);
+          if (u >= 1) grads(u - 1);
         }
-        tc_commit(s_full + h);
-        if (u >= 1) grads(u - 1);
+        if (n_u > 0) grads(n_u - 1);
+        U0 += n_u;
+        units += n_u;
       }
-      if (n_u > 0) grads(n_u - 1);
 #if FSP_BWD_TIMING
       tw[7] = clock64() - t_start;
       for (int i = 0; i < 8; ++i) atomicAdd(&g_bwd_wait[i], (unsigned long long)tw[i]);
-      atomicAdd(&g_bwd_wait[8], (unsigned long long)n_u);
+      atomicAdd(&g_bwd_wait[8], (unsigned long long)units);
       __threadfence();
       if (atomicAdd(&g_bwd_done, 1u) == gridDim.x - 1) {
         printf("bwd MMA issuer cycles (sum over CTAs): units %llu total %llu | ring_full(Q) %llu "
@@ -668,9 +746,16 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     const uint32_t ch = cw >> 2;               // which kV2Cols of the 64 columns
     const int r = quad * 32 + lane;            // kv row of S^T / dP^T
     const uint32_t lane_addr = (quad * 32u) << 16;
-    const int kv_pos = kv0 + r;
     const float sl2 = p.scale_log2;
     const int ctid = cw * 32 + lane;
+    uint32_t IT0 = 0;  // global index of the entry's first query tile
+    for (int k = 0;; ++k) {
+    const int w = bwd_take<kPersistent, true>(ering, k);
+    if (w >= p.n_tiles) break;
+    const KvTile T = decode_kv(p, w);
+    const int head = T.head, seq_start = T.seq_start, seqlen = T.seqlen, kt = T.kt,
+              kv0 = T.kv0, n_it = T.n_it;
+    const int kv_pos = kv0 + r;
     // statistics of query tile `it`: thread ctid < 128 owns lse row ctid, others delta
     auto load_stat = [&](int it) -> float {
       const int t = ctid & 127;
@@ -682,14 +767,14 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     };
     auto half = [&](auto diag_c, int it, int h) {
       constexpr bool kDiag = decltype(diag_c)::value;
-      const int buf = it & 1;
+      const int buf = (IT0 + it) & 1;
       const int c0 = h * 64 + ch * kV2Cols;  // query column offset inside the 128-row tile
       const float* ls = lse_s + buf * 128 + c0;
       const float* dl = delta_s + buf * 128 + c0;
 #if FSP_BWD_TIMING
       const long long tq0 = clock64();
 #endif
-      mbar_wait(s_full + h, it & 1);
+      mbar_wait(s_full + h, (IT0 + it) & 1);
 #if FSP_BWD_TIMING
       if (cw == 0 && lane == 0) atomicAdd(&g_bwd_wait[9], (unsigned long long)(clock64() - tq0));
 #endif
@@ -764,7 +849,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     float stat = (n_it > 0 && stat_thread) ? load_stat(0) : 0.f;
     for (int it = 0; it < n_it; ++it) {
       if (stat_thread) {
-        (ctid < 128 ? lse_s : delta_s)[(it & 1) * 128 + (ctid & 127)] = stat;
+        (ctid < 128 ? lse_s : delta_s)[((IT0 + it) & 1) * 128 + (ctid & 127)] = stat;
         if (it + 1 < n_it) stat = load_stat(it + 1);  // latency hidden behind this tile
       }
       named_bar_sync(1, 32 * kV2Compute);
@@ -777,11 +862,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       }
     }
     // ---- epilogue: this thread writes D/kCW columns of dK (scaled) and dV for kv row r
-    if (n_u > 0) mbar_wait(acc_done, 0);  // all MMAs done
+    mbar_wait(acc_done, k & 1);  // all MMAs of this entry done
     tc_fence_after();
     constexpr int kEpi = D / (kV2Compute / 4);  // dK/dV columns per compute thread
     const bool kvalid = kv_pos < seqlen;
-    if (p.sc.degree) {
+    if (!kPersistent && p.sc.degree) {  // (never combined with the persistent launch: the
+      // staging below borrows the Q/dO ring, which a persistent CTA refills for its next entry)
       // Fused head->seq (Eq. 4) of dK / dV (destination matrices 1 / 2).  A row's columns
       // are spread over 4 warps, and per-thread 16-byte stores would cross NVLink as
       // scattered small packets, so the tile is staged in shared memory (the Q/dO ring,
@@ -852,6 +938,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         }
       }
     }
+    IT0 += n_it;
+    }  // schedule entries
   } else {
     // ------------------------------------------------------------ dQ reduction warps
     // dQ^T(u) in TMEM: lane = d, columns = the half tile's 64 query rows.  dq_accum is
@@ -861,13 +949,20 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     const int part = (int)(warp - 2 - kV2Compute) >> 2;  // which kV2RedCols of the 64 columns
     const int r = quad * 32 + lane;
     const uint32_t lane_addr = (quad * 32u) << 16;
-    float* head_base = p.dq_accum + ((int64_t)head * p.total_rows + seq_start) * D + r;
+    uint32_t U0 = 0;  // global unit index of the entry's first unit
+    for (int k = 0;; ++k) {
+    const int w = bwd_take<kPersistent, true>(ering, k);
+    if (w >= p.n_tiles) break;
+    const KvTile T = decode_kv(p, w);
+    const int kt = T.kt, seqlen = T.seqlen, n_u = T.n_u;
+    float* head_base = p.dq_accum + ((int64_t)T.head * p.total_rows + T.seq_start) * D + r;
     for (int u = 0; u < n_u; ++u) {
       const int it = u >> 1, h = u & 1;
+      const uint32_t IT = (U0 + u) >> 1;
 #if FSP_BWD_TIMING
       const long long tr0 = clock64();
 #endif
-      mbar_wait(dq_full + h, it & 1);
+      mbar_wait(dq_full + h, IT & 1);
 #if FSP_BWD_TIMING
       const long long tr1 = clock64();
       if (warp == 2 + kV2Compute && lane == 0) atomicAdd(&g_bwd_wait[11], (unsigned long long)(tr1 - tr0));
@@ -921,6 +1016,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       if (warp == 2 + kV2Compute && lane == 0) atomicAdd(&g_bwd_wait[12], (unsigned long long)(clock64() - tr1));
 #endif
     }
+    U0 += n_u;
+    }  // schedule entries
   }
   tc_fence_before();
   __syncthreads();
@@ -967,10 +1064,28 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     p.scale_log2 = a->softmax_scale * kLog2e;
     p.sc = sc;
     const int64_t grid = a->n_tiles;
+    p.n_tiles = a->n_tiles;
     if (D == 128) {
       const int smem = BwdSmemV2::kBytes + 1024;
-      FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attn_bwd_kernel_v2<<<(unsigned)grid, kV2Threads, smem, stream>>>(tq, tk, tv, tdo, p);
+      // Persistent launch (one CTA per SM, dynamic claims) unless the head->seq exchange is
+      // fused: its epilogue stages dK/dV in the Q/dO ring the next entry refills.
+      int sms = 0, dev = 0;
+      FSP_CUDA(cudaGetDevice(&dev));
+      FSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const char* env = getenv("FSP_BWD_PERSISTENT");
+      const bool persistent = sc.degree == 0 && !(env && env[0] == '0') && grid > sms;
+      if (persistent) {
+        void* ctr = nullptr;
+        FSP_CUDA(cudaGetSymbolAddress(&ctr, g_bwd_next));
+        FSP_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), stream));
+        FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel_v2<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attn_bwd_kernel_v2<true><<<(unsigned)sms, kV2Threads, smem, stream>>>(tq, tk, tv, tdo, p);
+      } else {
+        FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel_v2<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attn_bwd_kernel_v2<false><<<(unsigned)grid, kV2Threads, smem, stream>>>(tq, tk, tv, tdo, p);
+      }
     } else {
       const int smem = BwdSmem<D>::kBytes + 1024;
       FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

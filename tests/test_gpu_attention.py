@@ -136,3 +136,38 @@ def test_fwd_persistent_matches_classic(lengths, H, monkeypatch):
     sub = qkv[a:b].cpu()
     o_ref, _ = attention_fwd_ref(sub[:, 0], sub[:, 1], sub[:, 2], (cu[1:5] - cu[1]).astype(np.int32))
     assert (outs["1"][0][a:b].float().cpu() - o_ref).abs().max() <= 2e-2
+
+
+@pytest.mark.parametrize("lengths,H", [
+    ([20000, 1, 129, 3000, 256, 2048] + [1024] * 40, 4),
+    ([300] * 600, 2),
+])
+def test_bwd_persistent_matches_classic(lengths, H, monkeypatch):
+    """The persistent backward launch (one CTA per SM, dynamic claims, barrier phases and the
+    Q/dO ring running on across entries) gives the classic launch's dK / dV bit for bit and
+    dQ up to the order of its fp32 atomics."""
+    from paper_2412_01523_b200 import ops
+    cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32)
+    T = int(cu[-1])
+    g = torch.Generator().manual_seed(7)
+    qkv = torch.randn(T, 3, H, 128, generator=g).bfloat16().cuda()
+    dout = torch.randn(T, H, 128, generator=g).bfloat16().cuda()
+    sched = ops.AttnSchedule.build(cu, "cuda", H, head_dim=128)
+    assert sched.n_bwd > torch.cuda.get_device_properties(0).multi_processor_count
+    o, lse = ops.attn_fwd(qkv[:, 0], qkv[:, 1], qkv[:, 2], sched)
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("FSP_BWD_PERSISTENT", mode)
+        dq, dk, dv = ops.attn_bwd(qkv[:, 0], qkv[:, 1], qkv[:, 2], o, dout, lse, sched)
+        torch.cuda.synchronize()
+        res[mode] = (dq.clone(), dk.clone(), dv.clone())
+    assert torch.equal(res["0"][1], res["1"][1])
+    assert torch.equal(res["0"][2], res["1"][2])
+    torch.testing.assert_close(res["0"][0].float(), res["1"][0].float(), atol=2e-2, rtol=2e-2)
+    # the persistent result against the fp32 oracle on sequences 1..3
+    a, b = int(cu[1]), int(cu[4])
+    sub = qkv[a:b].cpu()
+    refs = attention_bwd_ref(sub[:, 0], sub[:, 1], sub[:, 2], dout[a:b].cpu(),
+                             (cu[1:5] - cu[1]).astype(np.int32))
+    for got, ref in zip(res["1"], refs):
+        torch.testing.assert_close(got[a:b].float().cpu(), ref, atol=5e-2, rtol=5e-2)
