@@ -488,15 +488,16 @@ __device__ __forceinline__ KvTile decode_kv(const BwdParams& p, int w) {
   return t;
 }
 
-// Dynamic schedule of the persistent launch (as in the forward): the TMA producer claims
-// entries with an atomic on a per-device counter zeroed by the host before the launch and
-// hands them to the other roles through a two-slot shared-memory ring.
-__device__ int g_bwd_next;
-
+// Dynamic schedule of the persistent launch (as in the forward): one CTA per schedule
+// entry, and a CTA that finishes an entry steals the next not-yet-launched CTA's entry
+// through cluster launch control; the TMA producer hands entries to the other roles through
+// a two-slot shared-memory ring.
 struct BwdEntryRing {
   int* idx;
   uint64_t* full;
   uint64_t* empty;
+  void* resp;     // 16-byte cluster-launch-control response
+  uint64_t* clc;  // its completion barrier
 };
 constexpr int kBwdRingConsumers = 1 + kV2Compute + kV2Reduce;  // MMA thread + warps
 
@@ -505,7 +506,11 @@ __device__ __forceinline__ int bwd_claim(const BwdEntryRing& r, int k) {
   if (!kPersistent) return k == 0 ? (int)blockIdx.x : INT_MAX;
   const int slot = k & 1;
   mbar_wait(r.empty + slot, ((k >> 1) & 1) ^ 1);
-  const int w = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(&g_bwd_next, 1);
+  int w = (int)blockIdx.x;
+  if (k > 0) {
+    w = clc_steal(r.resp, r.clc, (k - 1) & 1);
+    if (w < 0) w = INT_MAX;
+  }
   r.idx[slot] = w;
   mbar_arrive(r.full + slot);
   return w;
@@ -544,7 +549,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* bar_kv = bars + 0;
   constexpr int kR = L::kSlots;
-  static_assert(1 + 2 * kR + 15 <= 32, "barrier region holds 32 mbarriers");
+  static_assert(1 + 2 * kR + 18 <= 32, "barrier region holds 32 mbarriers");
   uint64_t* ring_full = bars + 1;            // [kSlots]
   uint64_t* ring_empty = bars + 1 + kR;      // [kSlots]
   uint64_t* s_full = bars + 1 + 2 * kR;      // [2]
@@ -552,8 +557,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   uint64_t* dq_full = s_full + 4;            // [2]
   uint64_t* tm_free = s_full + 6;            // [2]
   uint64_t* acc_done = s_full + 8;           // dK / dV final
-  const BwdEntryRing ering{reinterpret_cast<int*>(s_full + 13), s_full + 9, s_full + 11};
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 14);
+  // s_full + 15 is 16-byte aligned: 1 + 2 * kSlots (even) + 2 + 15 words from a 1 KB boundary
+  static_assert((1 + 2 * kR + 15) % 2 == 0, "CLC response must be 16-byte aligned");
+  const BwdEntryRing ering{reinterpret_cast<int*>(s_full + 13), s_full + 9, s_full + 11,
+                           s_full + 15, s_full + 14};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 17);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -572,6 +580,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       mbar_init(ering.full + i, 1);
       mbar_init(ering.empty + i, kBwdRingConsumers);
     }
+    mbar_init(ering.clc, 1);
     mbar_init(acc_done, 1);
     fence_mbar_init();
   }
@@ -1067,20 +1076,14 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     p.n_tiles = a->n_tiles;
     if (D == 128) {
       const int smem = BwdSmemV2::kBytes + 1024;
-      // Persistent launch (one CTA per SM, dynamic claims) unless the head->seq exchange is
-      // fused: its epilogue stages dK/dV in the Q/dO ring the next entry refills.
-      int sms = 0, dev = 0;
-      FSP_CUDA(cudaGetDevice(&dev));
-      FSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      // Persistent launch (CTAs steal not-yet-launched entries) unless the head->seq exchange
+      // is fused: its epilogue stages dK/dV in the Q/dO ring the next entry refills.
       const char* env = getenv("FSP_BWD_PERSISTENT");
-      const bool persistent = sc.degree == 0 && !(env && env[0] == '0') && grid > sms;
+      const bool persistent = sc.degree == 0 && !(env && env[0] == '0');
       if (persistent) {
-        void* ctr = nullptr;
-        FSP_CUDA(cudaGetSymbolAddress(&ctr, g_bwd_next));
-        FSP_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), stream));
         FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel_v2<true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attn_bwd_kernel_v2<true><<<(unsigned)sms, kV2Threads, smem, stream>>>(tq, tk, tv, tdo, p);
+        attn_bwd_kernel_v2<true><<<(unsigned)grid, kV2Threads, smem, stream>>>(tq, tk, tv, tdo, p);
       } else {
         FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel_v2<false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -372,26 +372,32 @@ __device__ __forceinline__ PairTile decode_pair(const FwdParams& p, int w) {
   return t;
 }
 
-// Dynamic schedule of the persistent pair kernel: the TMA producer claims the next entry of
-// the longest-first schedule with an atomic on a per-device counter (zeroed by the host before
-// each launch) and hands it to the MMA and softmax warps through a two-slot ring in shared
-// memory — the persistent version of the hardware's "next CTA to the first free SM".
-__device__ int g_fwd_pair_next;
-
+// Dynamic schedule of the persistent pair kernel (cluster launch control): the grid still
+// has one CTA per schedule entry, but a CTA that finishes an entry cancels the next
+// not-yet-launched CTA (hardware launch order = the longest-first schedule order) and runs
+// its entry itself — the hardware's "next CTA to the first free SM" without the per-CTA
+// prologue / epilogue.  The TMA producer steals and hands each entry to the MMA and softmax
+// warps through a two-slot ring in shared memory.
 struct EntryRing {
   int* idx;         // [2] claimed schedule entries
   uint64_t* full;   // [2] producer -> consumers
   uint64_t* empty;  // [2] consumers (MMA thread + 8 softmax warps) -> producer
+  void* resp;       // 16-byte cluster-launch-control response
+  uint64_t* clc;    // its completion barrier
 };
 constexpr int kRingConsumers = 9;
 
-// Producer side: the k-th entry of this CTA (first: blockIdx.x; then claimed dynamically).
+// Producer side: the k-th entry of this CTA (its own first, then stolen ones).
 template <bool kPersistent>
 __device__ __forceinline__ int claim_entry(const EntryRing& r, int k) {
   if (!kPersistent) return k == 0 ? (int)blockIdx.x : INT_MAX;
   const int slot = k & 1;
   mbar_wait(r.empty + slot, ((k >> 1) & 1) ^ 1);
-  const int w = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(&g_fwd_pair_next, 1);
+  int w = (int)blockIdx.x;
+  if (k > 0) {
+    w = clc_steal(r.resp, r.clc, (k - 1) & 1);
+    if (w < 0) w = INT_MAX;
+  }
   r.idx[slot] = w;
   mbar_arrive(r.full + slot);
   return w;
@@ -433,8 +439,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   uint64_t* o_done = bars + 13;  // [2] per tile
   uint64_t* p_half = bars + 15;  // [2 tiles][2 halves]: P columns for kv rows 0-63 / 64-127
   uint64_t* q_empty = bars + 19; // Q_A / Q_B read by the last QK^T of a schedule entry
-  const EntryRing ring{reinterpret_cast<int*>(bars + 24), bars + 20, bars + 22};
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
+  const EntryRing ring{reinterpret_cast<int*>(bars + 24), bars + 20, bars + 22, bars + 26,
+                       bars + 25};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -447,6 +454,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       mbar_init(ring.full + i, 1);
       mbar_init(ring.empty + i, kRingConsumers);
     }
+    mbar_init(ring.clc, 1);
     mbar_init(bar_q, 1);
     for (int i = 0; i < L::kKStages; ++i) {
       mbar_init(k_full + i, 1);
@@ -924,21 +932,15 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   p.n_tiles = a->n_tiles;
   if (D == 128) {  // schedule entries are 256-row tile pairs (fsp_attn_schedule, head_dim 128)
     const int smem = Fwd2Smem::kBytes + 1024;
-    // Persistent launch (one CTA per SM walking the schedule, so an entry's Q load and first
+    // Persistent launch (CTAs steal not-yet-launched entries, so an entry's Q load and first
     // QK^T overlap the previous entry's softmax tail and epilogue) unless the head->seq
     // exchange is fused, whose epilogue stages rows in the entry's Q buffer.
-    int sms = 0, dev = 0;
-    FSP_CUDA(cudaGetDevice(&dev));
-    FSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const char* env = getenv("FSP_FWD_PERSISTENT");
-    const bool persistent = p.sc.degree == 0 && !(env && env[0] == '0') && a->n_tiles > sms;
+    const bool persistent = p.sc.degree == 0 && !(env && env[0] == '0');
     if (persistent) {
-      void* ctr = nullptr;
-      FSP_CUDA(cudaGetSymbolAddress(&ctr, g_fwd_pair_next));
-      FSP_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), stream));
       FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel<true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attn_fwd_pair_kernel<true><<<(unsigned)sms, kF2Threads, smem, stream>>>(tq, tk, tv, p);
+      attn_fwd_pair_kernel<true><<<(unsigned)a->n_tiles, kF2Threads, smem, stream>>>(tq, tk, tv, p);
     } else {
       FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel<false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -74,6 +74,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- cluster launch control
+// Persistent CTAs with hardware scheduling (sm_100): cancel a not-yet-launched CTA of this
+// grid and take over its work.  One thread issues it; the 16-byte response lands in `resp`
+// (16-byte aligned shared memory) and completes `bar` (armed with 16 bytes of tx).
+// Returns the cancelled CTA's blockIdx.x, or -1 when no CTA was left to cancel.
+__device__ __forceinline__ int clc_steal(void* resp, uint64_t* bar, uint32_t parity) {
+  mbar_expect_tx(bar, 16);
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 "
+      "[%0], [%1];" ::"r"(smem_u32(resp)), "r"(smem_u32(bar))
+      : "memory");
+  mbar_wait(bar, parity);
+  uint64_t rx, ry;
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(rx), "=l"(ry) : "r"(smem_u32(resp))
+               : "memory");
+  uint32_t canceled, cta;
+  asm volatile(
+      "{\n\t.reg .b128 R;\n\tmov.b128 R, {%2, %3};\n\t.reg .pred P;\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 P, R;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t"
+      "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, R;\n\t}"
+      : "=r"(canceled), "=r"(cta)
+      : "l"(rx), "l"(ry));
+  return canceled ? (int)cta : -1;
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
