@@ -602,7 +602,15 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         const int w = bwd_claim<kPersistent>(ering, k);
         if (w >= p.n_tiles) break;
         const KvTile T = decode_kv(p, w);
-        if (k > 0) mbar_wait(acc_done, (k - 1) & 1);  // the previous entry's MMAs read K / V
+        if (k > 0) {
+          // K / V of a kv tile are read by this CTA only (cold in L2): start their DRAM
+          // reads now, while the previous entry's last units still run
+          for (int b = 0; b < 2; ++b) {
+            tma_prefetch_l2_3d(&tm_k, b * 64, T.head, T.seq_start + T.kv0);
+            tma_prefetch_l2_3d(&tm_v, b * 64, T.head, T.seq_start + T.kv0);
+          }
+          mbar_wait(acc_done, (k - 1) & 1);  // the previous entry's MMAs read K / V
+        }
         mbar_expect_tx(bar_kv, 2 * L::kTileBytes);
         for (int b = 0; b < 2; ++b) {
           tma_load_3d(smem + L::kK + b * 16384, &tm_k, bar_kv, b * 64, T.head, T.seq_start + T.kv0);

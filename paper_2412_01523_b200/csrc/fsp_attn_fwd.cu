@@ -487,7 +487,17 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         const int w = claim_entry<kPersistent>(ring, k);
         if (w >= p.n_tiles) break;
         const PairTile T = decode_pair(p, w);
-        if (k > 0) mbar_wait(q_empty, (k - 1) & 1);  // previous entry's QK^T MMAs are done
+        if (k > 0) {
+          // Q rows of an entry are read by this CTA only: warm L2 while the previous entry
+          // finishes, and K_0 / V_0 with them
+          for (int b = 0; b < 2; ++b) {
+            tma_prefetch_l2_3d(&tm_q, b * 64, T.head, T.seq_start + T.q0);
+            if (T.has_b) tma_prefetch_l2_3d(&tm_q, b * 64, T.head, T.seq_start + T.q0 + 128);
+            tma_prefetch_l2_3d(&tm_k, b * 64, T.head, T.seq_start);
+            tma_prefetch_l2_3d(&tm_v, b * 64, T.head, T.seq_start);
+          }
+          mbar_wait(q_empty, (k - 1) & 1);  // previous entry's QK^T MMAs are done
+        }
         mbar_expect_tx(bar_q, (T.has_b ? 2 : 1) * L::kTileBytes);
         for (int b = 0; b < 2; ++b) {
           tma_load_3d(smem + L::kQA + b * 16384, &tm_q, bar_q, b * 64, T.head, T.seq_start + T.q0);
