@@ -130,3 +130,45 @@ def test_layout_check_on_every_golden_plan(lib):
             for g in lay.groups:
                 for j in range(g.degree):
                     ops.layout_check(g.pack_index(j), int((g.shard(j) >= 0).sum()))
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """The ctypes mirrors in capi.py have the C header's sizes and field offsets (a C
+    program compiled against include/flexsp_b200.h prints them) — ABI 4 appended an
+    FspHeadScatter to both attention argument structs."""
+    import shutil
+    import subprocess
+    from paper_2412_01523_b200 import capi
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    checks = {
+        "FspA2A": ["degree", "rows_per_rank", "src_stride", "dst_stride", "head_begin"],
+        "FspHeadScatter": ["degree", "head_offset", "dst_stride", "mat_stride", "d_unpack",
+                           "peer_dst"],
+        "FspAttnFwd": ["q", "lse", "o_stride", "d_seq_starts", "n_tiles", "softmax_scale",
+                       "scatter"],
+        "FspAttnBwd": ["dout", "dv", "dv_stride", "dq_accum", "d_tiles", "softmax_scale",
+                       "scatter"],
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "flexsp_b200.h"',
+             "int main(void) {"]
+    for st, fields in checks.items():
+        lines.append(f'  printf("{st} size %zu\\n", sizeof({st}));')
+        for f in fields:
+            lines.append(f'  printf("{st} {f} %zu\\n", offsetof({st}, {f}));')
+    lines.append("  return 0;\n}")
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "abi"
+    subprocess.run([cc, "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    got = {}
+    for line in out.splitlines():
+        st, field, val = line.split()
+        got[(st, field)] = int(val)
+    for st, fields in checks.items():
+        cls = getattr(capi, st)
+        assert ctypes.sizeof(cls) == got[(st, "size")], st
+        for f in fields:
+            assert getattr(cls, f).offset == got[(st, f)], (st, f)
