@@ -226,12 +226,10 @@ class FlexSPExecutor:
     # ------------------------------------------------------------ one micro-batch
     def local_buffers(self, sp: StepPlan, mb: RankMicroBatch):
         """Views of this rank's output buffers for micro-batch `mb` (inside the heap)."""
-        hd = self.n_heads * self.head_dim
         out = self.heap.view(sp.offsets["out_local"], (mb.n_local, self.n_heads, self.head_dim),
                              torch.bfloat16)
         dqkv = self.heap.view(sp.offsets["dqkv_local"], (mb.n_local, 3, self.n_heads, self.head_dim),
                               torch.bfloat16)
-        del hd
         return out, dqkv
 
     def micro_batch_forward(self, sp: StepPlan, mb: RankMicroBatch, qkv_local: torch.Tensor):

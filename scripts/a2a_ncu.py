@@ -15,7 +15,6 @@ launch shows one sender's NVLink TX bytes and duration.
 """
 import argparse
 import json
-import os
 import sys
 from pathlib import Path
 

@@ -1,5 +1,5 @@
 """Quick attention-kernel timing at the C2 shape (dev tool, not the bench)."""
-import sys, os, math, json
+import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2412_01523_b200 import ops
