@@ -298,13 +298,24 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // A quarter of the exponentials run as a degree-3 polynomial on the FMA pipe (the
 // 16/clk/SM MUFU.EX2 rate would otherwise equal the tensor-core time per tile).
 // TMEM: S_A|P_A [0,128) S_B|P_B [128,256) O_A [256,384) O_B [384,512).
-constexpr int kF2Threads = 64 + 256;
+// FSP_FWD_WG3: three warpgroups (TMA + MMA warps and two idle warps | softmax A | softmax B)
+// so setmaxnreg can move registers from the first to the softmax warpgroups, which then
+// hold a whole 128-column S row and read it from TMEM once per tile.
+#ifndef FSP_FWD_WG3
+#define FSP_FWD_WG3 1
+#endif
+constexpr int kF2Threads = FSP_FWD_WG3 ? 128 + 256 : 64 + 256;
+constexpr int kF2SoftmaxWarp0 = FSP_FWD_WG3 ? 4 : 2;
 #ifndef FSP_ABLATE_EXP
 #define FSP_ABLATE_EXP 0
 #endif
 // one exponential pair in FSP_POLY_EVERY runs as a polynomial on the FMA pipe (0 = none)
 #ifndef FSP_FWD_PREFETCH
 #define FSP_FWD_PREFETCH 1  // 1: TMEM load of the next 32-column chunk overlaps this chunk's math
+#endif
+#if FSP_FWD_WG3  // the row is loaded whole: no chunk prefetch
+#undef FSP_FWD_PREFETCH
+#define FSP_FWD_PREFETCH 0
 #endif
 #ifndef FSP_POLY_EVERY
 #define FSP_POLY_EVERY 4
@@ -476,168 +487,178 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      uint32_t g0 = 0;  // K/V ring position: kv steps issued by this CTA so far
-      for (int k = 0;; ++k) {
-        const int w = claim_entry<kPersistent>(ring, k);
-        if (w >= p.n_tiles) break;
-        const PairTile T = decode_pair(p, w);
-        if (k > 0) {
-          // Q rows of an entry are read by this CTA only: warm L2 while the previous entry
-          // finishes, and K_0 / V_0 with them
+  // Register reallocation is per warpgroup, so the role branches split at warpgroup
+  // granularity first (FSP_FWD_WG3: 128 x 56 + 256 x 208 of the 65,536 registers).
+  if (warp < kF2SoftmaxWarp0) {
+#if FSP_FWD_WG3
+    setmaxnreg_dec<56>();
+#endif
+    if (warp == 0) {
+      // ------------------------------------------------------------ TMA producer
+      if (elect_one()) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        uint32_t g0 = 0;  // K/V ring position: kv steps issued by this CTA so far
+        for (int k = 0;; ++k) {
+          const int w = claim_entry<kPersistent>(ring, k);
+          if (w >= p.n_tiles) break;
+          const PairTile T = decode_pair(p, w);
+          if (k > 0) {
+            // Q rows of an entry are read by this CTA only: warm L2 while the previous entry
+            // finishes, and K_0 / V_0 with them
+            for (int b = 0; b < 2; ++b) {
+              tma_prefetch_l2_3d(&tm_q, b * 64, T.head, T.seq_start + T.q0);
+              if (T.has_b) tma_prefetch_l2_3d(&tm_q, b * 64, T.head, T.seq_start + T.q0 + 128);
+              tma_prefetch_l2_3d(&tm_k, b * 64, T.head, T.seq_start);
+              tma_prefetch_l2_3d(&tm_v, b * 64, T.head, T.seq_start);
+            }
+            mbar_wait(q_empty, (k - 1) & 1);  // previous entry's QK^T MMAs are done
+          }
+          mbar_expect_tx(bar_q, (T.has_b ? 2 : 1) * L::kTileBytes);
           for (int b = 0; b < 2; ++b) {
-            tma_prefetch_l2_3d(&tm_q, b * 64, T.head, T.seq_start + T.q0);
-            if (T.has_b) tma_prefetch_l2_3d(&tm_q, b * 64, T.head, T.seq_start + T.q0 + 128);
-            tma_prefetch_l2_3d(&tm_k, b * 64, T.head, T.seq_start);
-            tma_prefetch_l2_3d(&tm_v, b * 64, T.head, T.seq_start);
+            tma_load_3d(smem + L::kQA + b * 16384, &tm_q, bar_q, b * 64, T.head, T.seq_start + T.q0);
+            if (T.has_b)
+              tma_load_3d(smem + L::kQB + b * 16384, &tm_q, bar_q, b * 64, T.head,
+                          T.seq_start + T.q0 + 128);
           }
-          mbar_wait(q_empty, (k - 1) & 1);  // previous entry's QK^T MMAs are done
+          // issue order K_0, K_1, V_0, K_2, V_1, ...: K is consumed one step before V
+          auto load_k = [&](int j) {
+            const uint32_t g = g0 + j;
+            const int st = g % L::kKStages;
+            mbar_wait(k_empty + st, ((g / L::kKStages) & 1) ^ 1);
+            mbar_expect_tx(k_full + st, L::kTileBytes);
+            for (int b = 0; b < 2; ++b)
+              tma_load_3d(smem + L::kK + st * L::kTileBytes + b * 16384, &tm_k, k_full + st, b * 64,
+                          T.head, T.seq_start + j * 128);
+          };
+          load_k(0);
+          for (int j = 0; j < T.n_kv; ++j) {
+            if (j + 1 < T.n_kv) load_k(j + 1);
+            const uint32_t g = g0 + j;
+            const int st = g & 1;
+            mbar_wait(v_empty + st, ((g >> 1) & 1) ^ 1);
+            mbar_expect_tx(v_full + st, L::kTileBytes);
+            for (int b = 0; b < 2; ++b)
+              tma_load_3d(smem + L::kV + st * L::kTileBytes + b * 16384, &tm_v, v_full + st, b * 64,
+                          T.head, T.seq_start + j * 128);
+          }
+          g0 += T.n_kv;
         }
-        mbar_expect_tx(bar_q, (T.has_b ? 2 : 1) * L::kTileBytes);
-        for (int b = 0; b < 2; ++b) {
-          tma_load_3d(smem + L::kQA + b * 16384, &tm_q, bar_q, b * 64, T.head, T.seq_start + T.q0);
-          if (T.has_b)
-            tma_load_3d(smem + L::kQB + b * 16384, &tm_q, bar_q, b * 64, T.head,
-                        T.seq_start + T.q0 + 128);
-        }
-        // issue order K_0, K_1, V_0, K_2, V_1, ...: K is consumed one step before V
-        auto load_k = [&](int j) {
-          const uint32_t g = g0 + j;
-          const int st = g % L::kKStages;
-          mbar_wait(k_empty + st, ((g / L::kKStages) & 1) ^ 1);
-          mbar_expect_tx(k_full + st, L::kTileBytes);
-          for (int b = 0; b < 2; ++b)
-            tma_load_3d(smem + L::kK + st * L::kTileBytes + b * 16384, &tm_k, k_full + st, b * 64,
-                        T.head, T.seq_start + j * 128);
-        };
-        load_k(0);
-        for (int j = 0; j < T.n_kv; ++j) {
-          if (j + 1 < T.n_kv) load_k(j + 1);
-          const uint32_t g = g0 + j;
-          const int st = g & 1;
-          mbar_wait(v_empty + st, ((g >> 1) & 1) ^ 1);
-          mbar_expect_tx(v_full + st, L::kTileBytes);
-          for (int b = 0; b < 2; ++b)
-            tma_load_3d(smem + L::kV + st * L::kTileBytes + b * 16384, &tm_v, v_full + st, b * 64,
-                        T.head, T.seq_start + j * 128);
-        }
-        g0 += T.n_kv;
       }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (elect_one()) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
-      constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
-      const uint32_t qa = smem_u32(smem + L::kQA), qb = smem_u32(smem + L::kQB);
-      const uint32_t k_base = smem_u32(smem + L::kK);
-      const uint32_t v_base = smem_u32(smem + L::kV);
+      __syncwarp();
+    } else if (warp == 1) {
+      // ------------------------------------------------------------ MMA issuer
+      if (elect_one()) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+        constexpr uint32_t idesc_o = make_idesc_bf16(128, D, false, true);
+        const uint32_t qa = smem_u32(smem + L::kQA), qb = smem_u32(smem + L::kQB);
+        const uint32_t k_base = smem_u32(smem + L::kK);
+        const uint32_t v_base = smem_u32(smem + L::kV);
 #if FSP_FWD_TIMING
-      long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      const long long t_start = clock64();
+        long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const long long t_start = clock64();
 #endif
-      uint32_t g0 = 0;                 // K/V ring position (kv steps consumed so far)
-      uint32_t p_cnt[2] = {0u, 0u};    // p_half completions consumed per tile x
-      int steps = 0;
-      for (int k = 0;; ++k) {
-        const int w = take_entry<kPersistent, false>(ring, k);
-        if (w >= p.n_tiles) break;
-        const PairTile T = decode_pair(p, w);
-        const int n_a = T.n_a, n_b = T.n_b, n_kv = T.n_kv;
-        int qk_left = n_a + n_b;  // QK^T groups still to issue; the last one frees Q_A / Q_B
-        FSP_FTW(5, mbar_wait(bar_q, k & 1));
-        auto qk = [&](int x, int j) {  // S_x = Q_x K_j^T
-          const uint32_t qbase = x ? qb : qa;
-          const uint32_t kb = k_base + ((g0 + j) % L::kKStages) * L::kTileBytes;
+        uint32_t g0 = 0;                 // K/V ring position (kv steps consumed so far)
+        uint32_t p_cnt[2] = {0u, 0u};    // p_half completions consumed per tile x
+        int steps = 0;
+        for (int k = 0;; ++k) {
+          const int w = take_entry<kPersistent, false>(ring, k);
+          if (w >= p.n_tiles) break;
+          const PairTile T = decode_pair(p, w);
+          const int n_a = T.n_a, n_b = T.n_b, n_kv = T.n_kv;
+          int qk_left = n_a + n_b;  // QK^T groups still to issue; the last one frees Q_A / Q_B
+          FSP_FTW(5, mbar_wait(bar_q, k & 1));
+          auto qk = [&](int x, int j) {  // S_x = Q_x K_j^T
+            const uint32_t qbase = x ? qb : qa;
+            const uint32_t kb = k_base + ((g0 + j) % L::kKStages) * L::kTileBytes;
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            mma_ss(tmem + x * 128, make_sdesc_sw128(qbase + off, 16, 1024),
-                   make_sdesc_sw128(kb + off, 16, 1024), idesc_s, kk > 0);
-          }
-          tc_commit(s_full + x);
-          if (--qk_left == 0) tc_commit(q_empty);
-        };
-        auto pv = [&](int x, int j) {  // O_x += P_x V_j, each half as soon as its P lands
-          const uint32_t vb = v_base + ((g0 + j) & 1) * L::kTileBytes;
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+              mma_ss(tmem + x * 128, make_sdesc_sw128(qbase + off, 16, 1024),
+                     make_sdesc_sw128(kb + off, 16, 1024), idesc_s, kk > 0);
+            }
+            tc_commit(s_full + x);
+            if (--qk_left == 0) tc_commit(q_empty);
+          };
+          auto pv = [&](int x, int j) {  // O_x += P_x V_j, each half as soon as its P lands
+            const uint32_t vb = v_base + ((g0 + j) & 1) * L::kTileBytes;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            FSP_FTW(x, mbar_wait(p_half + 2 * x + hh, (p_cnt[x] + j) & 1));
+            for (int hh = 0; hh < 2; ++hh) {
+              FSP_FTW(x, mbar_wait(p_half + 2 * x + hh, (p_cnt[x] + j) & 1));
+              tc_fence_after();
+#pragma unroll
+              for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
+                mma_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8,
+                       make_sdesc_sw128(vb + kk * 2048, 16384, 1024), idesc_o,
+                       (j > 0 || kk > 0) ? 1u : 0u);
+            }
+          };
+          auto wait_k = [&](int j) {
+            const uint32_t g = g0 + j;
+            FSP_FTW(2, mbar_wait(k_full + g % L::kKStages, (g / L::kKStages) & 1));
             tc_fence_after();
-#pragma unroll
-            for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
-              mma_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8,
-                     make_sdesc_sw128(vb + kk * 2048, 16384, 1024), idesc_o,
-                     (j > 0 || kk > 0) ? 1u : 0u);
-          }
-        };
-        auto wait_k = [&](int j) {
-          const uint32_t g = g0 + j;
-          FSP_FTW(2, mbar_wait(k_full + g % L::kKStages, (g / L::kKStages) & 1));
-          tc_fence_after();
-        };
-        wait_k(0);
-        qk(0, 0);
-        if (n_b > 0) qk(1, 0);
-        tc_commit(k_empty + g0 % L::kKStages);
-        for (int j = 0; j < n_kv; ++j) {
-          const uint32_t g = g0 + j;
-          const int st = g & 1;
-          const bool next = j + 1 < n_kv;
-          FSP_FTW(3, mbar_wait(v_full + st, (g >> 1) & 1));
-          if (j < n_a) {
-            pv(0, j);
-            if (j + 1 < n_a) {
-              wait_k(j + 1);
-              qk(0, j + 1);
-            } else {
-              tc_commit(o_done + 0);
+          };
+          wait_k(0);
+          qk(0, 0);
+          if (n_b > 0) qk(1, 0);
+          tc_commit(k_empty + g0 % L::kKStages);
+          for (int j = 0; j < n_kv; ++j) {
+            const uint32_t g = g0 + j;
+            const int st = g & 1;
+            const bool next = j + 1 < n_kv;
+            FSP_FTW(3, mbar_wait(v_full + st, (g >> 1) & 1));
+            if (j < n_a) {
+              pv(0, j);
+              if (j + 1 < n_a) {
+                wait_k(j + 1);
+                qk(0, j + 1);
+              } else {
+                tc_commit(o_done + 0);
+              }
             }
-          }
-          if (j < n_b) {
-            pv(1, j);
-            if (j + 1 < n_b) {
-              wait_k(j + 1);
-              qk(1, j + 1);
-            } else {
-              tc_commit(o_done + 1);
+            if (j < n_b) {
+              pv(1, j);
+              if (j + 1 < n_b) {
+                wait_k(j + 1);
+                qk(1, j + 1);
+              } else {
+                tc_commit(o_done + 1);
+              }
             }
+            tc_commit(v_empty + st);
+            if (next) tc_commit(k_empty + (g + 1) % L::kKStages);
           }
-          tc_commit(v_empty + st);
-          if (next) tc_commit(k_empty + (g + 1) % L::kKStages);
+          p_cnt[0] += n_a;
+          p_cnt[1] += n_b;
+          g0 += n_kv;
+          steps += n_a + n_b;
         }
-        p_cnt[0] += n_a;
-        p_cnt[1] += n_b;
-        g0 += n_kv;
-        steps += n_a + n_b;
-      }
 #if FSP_FWD_TIMING
-      tw[7] = clock64() - t_start;
-      for (int i = 0; i < 8; ++i) atomicAdd(&g_fwd_wait[i], (unsigned long long)tw[i]);
-      atomicAdd(&g_fwd_wait[8], (unsigned long long)steps);
-      __threadfence();
-      if (atomicAdd(&g_fwd_done, 1u) == gridDim.x - 1) {
-        printf("fwd MMA issuer cycles (sum over CTAs): tile-steps %llu total %llu | p_half A %llu "
-               "p_half B %llu k_full %llu v_full %llu q %llu\n", g_fwd_wait[8], g_fwd_wait[7],
-               g_fwd_wait[0], g_fwd_wait[1], g_fwd_wait[2], g_fwd_wait[3], g_fwd_wait[5]);
-        printf("fwd softmax warp (tile A, quad 0): s_full wait %llu busy %llu | to max %llu to "
-               "first-half release %llu\n", g_fwd_wait[9], g_fwd_wait[10], g_fwd_wait[11],
-               g_fwd_wait[12]);
-        for (int i = 0; i < 16; ++i) g_fwd_wait[i] = 0;
-        g_fwd_done = 0;
-      }
+        tw[7] = clock64() - t_start;
+        for (int i = 0; i < 8; ++i) atomicAdd(&g_fwd_wait[i], (unsigned long long)tw[i]);
+        atomicAdd(&g_fwd_wait[8], (unsigned long long)steps);
+        __threadfence();
+        if (atomicAdd(&g_fwd_done, 1u) == gridDim.x - 1) {
+          printf("fwd MMA issuer cycles (sum over CTAs): tile-steps %llu total %llu | p_half A %llu "
+                 "p_half B %llu k_full %llu v_full %llu q %llu\n", g_fwd_wait[8], g_fwd_wait[7],
+                 g_fwd_wait[0], g_fwd_wait[1], g_fwd_wait[2], g_fwd_wait[3], g_fwd_wait[5]);
+          printf("fwd softmax warp (tile A, quad 0): s_full wait %llu busy %llu | to max %llu to "
+                 "first-half release %llu\n", g_fwd_wait[9], g_fwd_wait[10], g_fwd_wait[11],
+                 g_fwd_wait[12]);
+          for (int i = 0; i < 16; ++i) g_fwd_wait[i] = 0;
+          g_fwd_done = 0;
+        }
 #endif
+      }
+      __syncwarp();
     }
-    __syncwarp();
   } else {
+#if FSP_FWD_WG3
+    setmaxnreg_inc<208>();
+#endif
     // ------------------------------------------------------------ softmax warpgroups
-    const int x = (warp - 2) >> 2;        // 0 -> tile A, 1 -> tile B
+    const int x = (warp - kF2SoftmaxWarp0) >> 2;  // 0 -> tile A, 1 -> tile B
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;
     const uint32_t lane_addr = (quad * 32u) << 16;
@@ -703,14 +724,22 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         // pass 1: row max; four independent FMNMX3 chains over chunked TMEM loads (the
         // whole 128-column row does not fit the 168-register budget of 10 warps per CTA)
         float mxs[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#if FSP_FWD_PREFETCH
+#if FSP_FWD_WG3
+        uint32_t sr[4][32];  // the whole S row, one TMEM round trip per tile
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_addr + s_col + 32 * c, sr[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_wait_tied(sr[c]);
+#elif FSP_FWD_PREFETCH
         uint32_t buf[2][32];  // chunk c+1 is in flight while chunk c is processed
         tmem_ld32(tmem + lane_addr + s_col, buf[0]);
         tmem_ld_wait_tied(buf[0]);
 #endif
 #pragma unroll
         for (int c = 0; c < 128; c += 32) {
-#if FSP_FWD_PREFETCH
+#if FSP_FWD_WG3
+          uint32_t(&r)[32] = sr[c / 32];
+#elif FSP_FWD_PREFETCH
           uint32_t(&r)[32] = buf[(c / 32) & 1];
           if (c + 32 < 128) tmem_ld32(tmem + lane_addr + s_col + c + 32, buf[((c / 32) + 1) & 1]);
 #else
@@ -768,7 +797,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 #pragma unroll
         for (int c = 0; c < 128; c += 32) {
           uint32_t pk[16];
-#if FSP_FWD_PREFETCH
+#if FSP_FWD_WG3
+          uint32_t(&r)[32] = sr[c / 32];
+#elif FSP_FWD_PREFETCH
           uint32_t(&r)[32] = buf[(c / 32) & 1];
           if (c + 32 < 128) tmem_ld32(tmem + lane_addr + s_col + c + 32, buf[((c / 32) + 1) & 1]);
 #else
