@@ -1,7 +1,6 @@
 """Calibration loop on CPU: the profile CSV this repo writes is the
 reference's ProfileRecord format, and the reference's own fit recovers known coefficients
 from records shaped like the B200 profiler's output."""
-import os
 import sys
 from pathlib import Path
 

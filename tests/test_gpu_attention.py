@@ -5,7 +5,6 @@ Tolerances (bf16 inputs, fp32 accumulation):
   LSE:  max |diff| <= 1e-3 * max(1, |lse|)
   dQ/dK/dV: allclose(atol=5e-2, rtol=5e-2) and cosine >= 0.999
 """
-import math
 
 import numpy as np
 import pytest

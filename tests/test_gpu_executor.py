@@ -4,7 +4,6 @@ Multi-rank exchanges are emulated on one GPU by calling every member's kernel in
 with peer pointers aimed at per-member buffers on the same device (the kernels are
 rank-local and never wait on each other, so this is safe on a single GPU).
 """
-import json
 from pathlib import Path
 
 import numpy as np
