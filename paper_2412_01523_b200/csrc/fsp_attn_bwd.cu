@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
 #endif
 constexpr int kV2Compute = FSP_BWD_COMPUTE_WARPS;  // 8 or 16: 2 or 4 warps per lane quadrant
 constexpr int kV2Cols = 64 / (kV2Compute / 4);      // query columns per compute warp
+static_assert(kV2Compute == 8 || kV2Compute == 16, "2 or 4 compute warps per TMEM lane quadrant");
 #ifndef FSP_BWD_REDUCE_WARPS
 #define FSP_BWD_REDUCE_WARPS 4
 #endif
