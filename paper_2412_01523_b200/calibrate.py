@@ -52,10 +52,13 @@ def step_bytes_per_device(lengths: Sequence[int], degree: int, n_heads: int, hea
     h = n_heads * head_dim
     shard = t_pad // degree
     b = shard * (3 + 1 + 1 + 3) * h * 2
-    hs = h // degree
+    # uneven head splits (52 heads at d=8 -> 7,...,6): every rank's head-sharded buffers
+    # are sized by the largest member's share, as FlexSPExecutor.prepare allocates them
+    heads = -(-n_heads // degree)
+    hs = heads * head_dim
     if degree > 1:
         b += t_pad * (3 + 1 + 1 + 3) * hs * 2
-    b += t_pad * hs * 4 + 2 * t_pad * (n_heads // degree) * 4  # dq_accum, lse, delta
+    b += t_pad * hs * 4 + 2 * t_pad * heads * 4  # dq_accum, lse, delta
     return float(b)
 
 

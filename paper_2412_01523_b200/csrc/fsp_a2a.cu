@@ -10,6 +10,8 @@
 // send by reading source rows through the permutation; the unpack is fused into the
 // receive side of head2seq the same way.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "fsp_host.h"
 
@@ -69,6 +71,7 @@ __global__ void __launch_bounds__(kThreads) a2a_kernel(const uint8_t* __restrict
       vpc = (int)(((a.head_begin[j + 1] - hb) * head_bytes) >> 4);
       const int32_t srow = index ? index[i] : (int32_t)i;
       zero = srow < 0;
+      if (!zero && src == nullptr) __trap();  // a live row behind a null src: caller bug
       sp = reinterpret_cast<const int4*>(src + (int64_t)(zero ? 0 : srow) * src_stride +
                                          m * full_row + hb * head_bytes);
       const int64_t drow = (int64_t)a.rank * a.rows_per_rank + i;
@@ -103,8 +106,18 @@ __global__ void __launch_bounds__(kThreads) a2a_kernel(const uint8_t* __restrict
   __threadfence_system();
 }
 
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Word of a rank's signal page where a timed-out barrier leaves its mark (the slots
+// proper are [0, 2 * world) at most).
+constexpr int kBarrierErrorWord = 1023;
+
 __global__ void group_barrier_kernel(PeerPtrs sig, int degree, int rank, int slot_base,
-                                     uint32_t epoch) {
+                                     uint32_t epoch, uint64_t timeout_ns) {
   const int t = threadIdx.x;
   if (t < degree) {
     __threadfence_system();
@@ -112,15 +125,45 @@ __global__ void group_barrier_kernel(PeerPtrs sig, int degree, int rank, int slo
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(sig.p[rank]) + slot_base + t;
     uint32_t seen;
+    const uint64_t t0 = global_ns();
+    uint32_t polls = 0;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(mine) : "memory");
+      // Bounded spin: a peer that never arrives (it raised on the host, died, or its
+      // stream is stuck) turns into a reported device fault instead of a hang that can
+      // only be cleared by killing every process of the job.
+      if ((int32_t)(seen - epoch) < 0 && timeout_ns && (++polls & 1023) == 0 &&
+          global_ns() - t0 > timeout_ns) {
+        reinterpret_cast<volatile uint32_t*>(sig.p[rank])[kBarrierErrorWord] =
+            0xBA000000u | ((uint32_t)(slot_base + t) << 8) | (uint32_t)(slot_base + rank);
+        printf("fsp_group_barrier: rank %d (slot base %d) timed out after %.1f s waiting for "
+               "member %d at epoch %u (saw %u)\n",
+               rank, slot_base, timeout_ns * 1e-9, t, epoch, seen);
+        __trap();
+      }
     } while ((int32_t)(seen - epoch) < 0);
   }
   __syncwarp();
 }
 
-int check_a2a(const FspA2A* a, const void* src, void* const* peer_dst) {
-  FSP_CHECK_ARG(a && src && peer_dst, "null pointer argument");
+// FSP_BARRIER_TIMEOUT_S (seconds, default 120; 0 = wait forever), read once per process.
+uint64_t barrier_timeout_ns() {
+  static const uint64_t ns = [] {
+    const char* e = getenv("FSP_BARRIER_TIMEOUT_S");
+    const double s = e ? atof(e) : 120.0;
+    return s > 0 ? (uint64_t)(s * 1e9) : (uint64_t)0;
+  }();
+  return ns;
+}
+
+template <bool kSeq2Head>
+int check_a2a(const FspA2A* a, const void* src, void* const* peer_dst, const int32_t* index) {
+  FSP_CHECK_ARG(a && peer_dst, "null pointer argument");
+  // src may be null only when nothing is read from it: no rows (an empty group), or a
+  // seq2head send whose shard rows are all padding (a member of a tiny group holding no
+  // tokens; its pack index is all -1, checked by fsp_layout_check on the host)
+  FSP_CHECK_ARG(src || a->rows_per_rank == 0 || (kSeq2Head && index),
+                "null src (allowed only for an empty exchange or an all-pad seq2head shard)");
   FSP_CHECK_ARG(a->degree >= 1 && a->degree <= kMaxDegree && (a->degree & (a->degree - 1)) == 0,
                 "degree must be a power of two in [1, 8] (got %d)", a->degree);
   FSP_CHECK_ARG(a->rank >= 0 && a->rank < a->degree, "rank %d outside group of %d", a->rank,
@@ -148,7 +191,7 @@ int check_a2a(const FspA2A* a, const void* src, void* const* peer_dst) {
 template <bool kSeq2Head>
 int launch_a2a(const FspA2A* a, const void* src, void* const* peer_dst, const int32_t* index,
                void* stream) {
-  int rc = check_a2a(a, src, peer_dst);
+  int rc = check_a2a<kSeq2Head>(a, src, peer_dst, index);
   if (rc) return rc;
   FspA2A n = *a;  // normalised copy: the even split spelled out
   if (n.head_begin[n.degree] == 0)
@@ -201,7 +244,8 @@ extern "C" int fsp_group_barrier(uint32_t* const* peer_signal, int32_t degree, i
     FSP_CHECK_ARG(peer_signal[j] != nullptr, "peer_signal[%d] null", j);
     pp.p[j] = reinterpret_cast<uint8_t*>(peer_signal[j]);
   }
-  group_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(pp, degree, rank, slot_base, epoch);
+  group_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(pp, degree, rank, slot_base, epoch,
+                                                            barrier_timeout_ns());
   FSP_LAUNCH_CHECK();
   return FSP_OK;
 }

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t lane = lane_id();
   const int tile = p.tiles[2 * blockIdx.x];
   const int head = p.tiles[2 * blockIdx.x + 1];
-  const int seq = tile >> 16;
+  const int seq = (int)((uint32_t)tile >> 16);  // unsigned: n_seq up to 65535
   const int kt = tile & 0xFFFF;
   const int seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
   const int seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
@@ -452,6 +452,10 @@ struct BwdSmemV2 {
   static constexpr int kBar = kStat + 4 * 128 * 4;
   static constexpr int kBytes = kBar + 256;
 };
+// The fused dK/dV epilogue stages its two 128-row output tiles (2 x 32 KB) in the Q/dO
+// ring, which is idle by then: the ring must hold at least that much.
+static_assert(BwdSmemV2::kSlots * BwdSmemV2::kHalfBytes >= 2 * BwdSmemV2::kTileBytes,
+              "FSP_BWD_RING too small for the dK/dV epilogue staging (needs >= 4 slots)");
 
 #ifndef FSP_BWD_TIMING
 #define FSP_BWD_TIMING 0  // profiling build: cycles the MMA issuer / compute warps spend waiting
@@ -478,7 +482,7 @@ __device__ __forceinline__ KvTile decode_kv(const BwdParams& p, int w) {
   KvTile t;
   const int tile = p.tiles[2 * w];
   t.head = p.tiles[2 * w + 1];
-  const int seq = tile >> 16;
+  const int seq = (int)((uint32_t)tile >> 16);  // unsigned: n_seq up to 65535
   t.kt = tile & 0xFFFF;
   t.seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
   t.seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
@@ -1125,6 +1129,11 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
 extern "C" int fsp_attn_bwd(const FspAttnBwd* a, void* stream) {
   using namespace fsp;
   FSP_CHECK_ARG(a != nullptr, "null args");
+  FSP_CHECK_ARG(a->head_dim == 64 || a->head_dim == 128, "head_dim must be 64 or 128 (got %d)",
+                a->head_dim);
+  FSP_CHECK_ARG(a->n_heads >= 1, "n_heads must be >= 1");
+  FSP_CHECK_ARG(a->total_rows >= 0 && a->n_tiles >= 0, "negative sizes");
+  if (a->total_rows == 0 && a->n_tiles == 0) return FSP_OK;  // empty group: no-op
   int rc = check_attn_common(a->q, a->k, a->v, a->q_stride, a->k_stride, a->v_stride,
                              a->d_cu_seqlens, a->d_tiles, a->n_tiles, a->n_seq, a->total_rows,
                              a->n_heads, a->head_dim);

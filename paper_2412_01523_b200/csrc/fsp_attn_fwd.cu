@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const uint32_t lane = lane_id();
   const int tile = p.tiles[2 * blockIdx.x];
   const int head = p.tiles[2 * blockIdx.x + 1];
-  const int seq = tile >> 16;
+  const int seq = (int)((uint32_t)tile >> 16);  // unsigned: n_seq up to 65535
   const int qt = tile & 0xFFFF;
   const int seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
   const int seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
@@ -371,7 +371,7 @@ __device__ __forceinline__ PairTile decode_pair(const FwdParams& p, int w) {
   PairTile t;
   const int tile = p.tiles[2 * w];
   t.head = p.tiles[2 * w + 1];
-  const int seq = tile >> 16;
+  const int seq = (int)((uint32_t)tile >> 16);  // unsigned: n_seq up to 65535
   const int pair = tile & 0xFFFF;
   t.seq_start = p.seq_starts ? p.seq_starts[seq] : p.cu_seqlens[seq];
   t.seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
@@ -1002,6 +1002,8 @@ int check_attn_common(const void* q, const void* k, const void* v, int64_t qs, i
   FSP_CHECK_ARG(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128 (got %d)", head_dim);
   FSP_CHECK_ARG(n_heads >= 1, "n_heads must be >= 1");
   FSP_CHECK_ARG(n_seq >= 0 && total_rows >= 0 && n_tiles >= 0, "negative sizes");
+  // tiles are {seq << 16 | tile} words decoded unsigned: at most 65535 sequences
+  FSP_CHECK_ARG(n_seq < 65536, "n_seq must be in [0, 65536) (got %d)", n_seq);
   FSP_CHECK_ARG(q && k && v && cu && (tiles || n_tiles == 0), "null pointer argument");
   FSP_CHECK_ARG(qs >= (int64_t)n_heads * head_dim && ks >= (int64_t)n_heads * head_dim &&
                     vs >= (int64_t)n_heads * head_dim,
@@ -1054,7 +1056,7 @@ extern "C" int32_t fsp_attn_schedule(const int32_t* cu, int32_t n_seq, int32_t n
     for (int h = 0; h < n_heads; ++h)
       for (int j = 0; j < nt; ++j) {
         const int t = kind == FSP_SCHED_BWD ? j : nt - 1 - j;
-        tiles[2 * k] = (s << 16) | t;
+        tiles[2 * k] = (int32_t)(((uint32_t)s << 16) | (uint32_t)t);
         tiles[2 * k + 1] = h;
         ++k;
       }
@@ -1066,6 +1068,13 @@ extern "C" int32_t fsp_attn_schedule(const int32_t* cu, int32_t n_seq, int32_t n
 extern "C" int fsp_attn_fwd(const FspAttnFwd* a, void* stream) {
   using namespace fsp;
   FSP_CHECK_ARG(a != nullptr, "null args");
+  // an empty group (no rows: a selected group without sequences, or a member holding
+  // only pad rows of a tiny one) is a no-op whatever its (possibly null) buffers are
+  FSP_CHECK_ARG(a->head_dim == 64 || a->head_dim == 128, "head_dim must be 64 or 128 (got %d)",
+                a->head_dim);
+  FSP_CHECK_ARG(a->n_heads >= 1, "n_heads must be >= 1");
+  FSP_CHECK_ARG(a->total_rows >= 0 && a->n_tiles >= 0, "negative sizes");
+  if (a->total_rows == 0 && a->n_tiles == 0) return FSP_OK;
   int rc = check_attn_common(a->q, a->k, a->v, a->q_stride, a->k_stride, a->v_stride,
                              a->d_cu_seqlens, a->d_tiles, a->n_tiles, a->n_seq, a->total_rows,
                              a->n_heads, a->head_dim);

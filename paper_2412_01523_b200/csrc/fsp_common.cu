@@ -132,7 +132,7 @@ namespace fsp {
 int scatter_from_abi(const FspHeadScatter& a, int n_mats, int n_heads, int head_dim,
                      int total_rows, ScatterDev* out) {
   *out = ScatterDev{};
-  if (a.degree == 0) return FSP_OK;
+  if (a.degree == 0 || total_rows == 0) return FSP_OK;  // nothing to scatter
   FSP_CHECK_ARG(a.degree >= 1 && a.degree <= 8, "scatter degree must be in 1..8 (got %d)",
                 a.degree);
   FSP_CHECK_ARG(a.rows_per_rank >= 1, "scatter rows_per_rank must be >= 1");

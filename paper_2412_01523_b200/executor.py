@@ -116,7 +116,7 @@ class FlexSPExecutor:
 
     def __init__(self, world_size: int, rank: int, n_heads: int, head_dim: int,
                  device: torch.device | str = "cuda", softmax_scale: float | None = None,
-                 group=None, fuse_head2seq: bool = True):
+                 group=None, fuse_head2seq: bool = True, heap_factory=None):
         if head_dim not in (64, 128):
             raise ValueError("head_dim must be 64 or 128")
         self.world_size = world_size
@@ -134,6 +134,10 @@ class FlexSPExecutor:
         # backward go straight to their owners' sequence shards); False = separate
         # fsp_a2a_head2seq launches after attention (kept for A/B measurements)
         self.fuse_head2seq = fuse_head2seq
+        # heap_factory(nbytes) -> PeerHeap-like (view / peer / nbytes); None = the
+        # symmetric-memory heap.  vranks.VirtualCluster passes per-virtual-rank heaps that
+        # live on one device (the single-GPU multi-rank harness).
+        self.heap_factory = heap_factory
 
     # ------------------------------------------------------------ planning -> tables
     def prepare(self, plan: Any, lengths: Sequence[int]) -> StepPlan:
@@ -199,7 +203,8 @@ class FlexSPExecutor:
         if self.heap is not None and self.heap.nbytes >= nbytes:
             return
         # collective when world_size > 1: every rank prepares the same plan
-        self.heap = PeerHeap(nbytes, self.device, self.world_size, self.group)
+        self.heap = (self.heap_factory(nbytes) if self.heap_factory is not None else
+                     PeerHeap(nbytes, self.device, self.world_size, self.group))
         self.epoch = 0
 
     def _workspace(self, name: str, numel: int, dtype: torch.dtype) -> torch.Tensor:

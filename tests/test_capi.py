@@ -39,7 +39,8 @@ def _schedule(lib, lens, rev, heads=1, head_dim=64):
     buf = np.zeros(max(2 * n, 2), dtype=np.int32)
     ptr = buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     assert lib.fsp_attn_schedule(p, len(lens), heads, head_dim, rev, ptr, n) == n
-    return [(int(buf[2 * i]) >> 16, int(buf[2 * i]) & 0xFFFF, int(buf[2 * i + 1])) for i in range(n)]
+    w = buf[0::2].view(np.uint32)  # tile words are {seq << 16 | tile}, decoded unsigned
+    return [(int(w[i]) >> 16, int(w[i]) & 0xFFFF, int(buf[2 * i + 1])) for i in range(n)]
 
 
 @pytest.mark.parametrize("rev", [0, 1])
@@ -60,6 +61,86 @@ def test_schedule_complete_and_ordered(lib, rev):
         for h in range(heads):
             costs = [(ntiles[s] - t) if rev else (t + 1) for t, hh in block if hh == h]
             assert costs == sorted(costs, reverse=True)
+
+
+def test_schedule_beyond_32768_sequences(lib):
+    """A group with more than 2^15 sequences (40,000 one-token sequences): the tile word's
+    sequence field is decoded unsigned, so every sequence index appears exactly once and
+    none comes back negative; 65,536 sequences are rejected."""
+    from paper_2412_01523_b200 import capi
+    for kind in (0, 1):
+        tiles = _schedule(lib, [1] * 40000, kind, heads=1, head_dim=128)
+        assert sorted(s for s, _, _ in tiles) == list(range(40000))
+        assert all(t == 0 for _, t, _ in tiles)
+    cu = np.arange(65537, dtype=np.int32)
+    assert lib.fsp_attn_schedule(cu.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 65536, 1,
+                                 128, 0, None, 0) == capi.FSP_ERR_INVALID
+
+
+def test_empty_group_calls_are_noops(lib):
+    """An empty group (no rows: a selected group without sequences) or a member holding
+    only pad rows is a valid no-op at the C-ABI even with null buffers, so such a rank
+    does not raise while its peers wait in the group barrier."""
+    from paper_2412_01523_b200 import capi
+    a = capi.FspAttnFwd()
+    a.head_dim, a.n_heads = 128, 4
+    assert lib.fsp_attn_fwd(ctypes.byref(a), None) == capi.FSP_OK
+    b = capi.FspAttnBwd()
+    b.head_dim, b.n_heads = 128, 4
+    b.scatter.degree, b.scatter.rows_per_rank = 2, 0
+    assert lib.fsp_attn_bwd(ctypes.byref(b), None) == capi.FSP_OK
+    x = capi.FspA2A(2, 1, 0, 3, 4, 64, 768, 384)  # R = 0: nothing to move, null src ok
+    ptrs = (ctypes.c_void_p * 2)(16, 16)
+    assert lib.fsp_a2a_seq2head(ctypes.byref(x), None, ptrs, None, None) == capi.FSP_OK
+    x.rows_per_rank = 2  # rows to send but no src and no index: rejected
+    assert lib.fsp_a2a_seq2head(ctypes.byref(x), None, ptrs, None, None) == capi.FSP_ERR_INVALID
+    assert lib.fsp_a2a_head2seq(ctypes.byref(x), None, ptrs, None, None) == capi.FSP_ERR_INVALID
+
+
+def test_integration_stub_matches_binding(lib):
+    """The reference-side ctypes stub printed in INTEGRATION.md §2 is executed against
+    the built library: its structures have capi.py's layouts, its argument lists equal
+    capi.py's, and the host-only entry points give the same answers through it."""
+    from paper_2412_01523_b200 import capi
+    text = (ROOT / "INTEGRATION.md").read_text()
+    sec = text[text.index("## 2. The ctypes stub"):]
+    code = sec[sec.index("```python\n") + 10:]
+    code = code[:code.index("```")]
+    code = code.replace('"paper_2412_01523_b200/_lib/libflexsp_b200.so"', repr(str(capi.LIB_PATH)))
+    ns: dict = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    stub = ns["lib"]
+    for st in ("FspA2A", "FspHeadScatter", "FspAttnFwd", "FspAttnBwd"):
+        mine, theirs = getattr(capi, st), ns[st]
+        assert ctypes.sizeof(mine) == ctypes.sizeof(theirs), st
+        assert [(f, getattr(mine, f).offset) for f, _ in mine._fields_] == \
+            [(f, getattr(theirs, f).offset) for f, _ in theirs._fields_], st
+
+    def sig(fn):
+        return [getattr(t, "__name__", str(t)) for t in (fn.argtypes or [])], \
+            getattr(fn.restype, "__name__", str(fn.restype))
+    for name in capi.EXPORTED:
+        if name == "fsp_selftest_umma":  # diagnostic, not part of the reference binding
+            continue
+        assert sig(getattr(stub, name)) == sig(getattr(lib, name)), name
+    lens = [5, 300, 1, 4096, 77]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    for kind in (0, 1):
+        p = cu.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        n = stub.fsp_attn_schedule(p, len(lens), 3, 128, kind, None, 0)
+        a = np.zeros(2 * n, dtype=np.int32)
+        b = np.zeros(2 * n, dtype=np.int32)
+        stub.fsp_attn_schedule(p, len(lens), 3, 128, kind,
+                               a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n)
+        lib.fsp_attn_schedule(p, len(lens), 3, 128, kind,
+                              b.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n)
+        assert n > 0 and np.array_equal(a, b)
+    idx = np.array([2, 0, -1, 1], dtype=np.int32)
+    ns["check"](stub.fsp_layout_check(idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 4, 3))
+    bad = np.array([0, 0], dtype=np.int32)
+    with pytest.raises(ValueError):
+        ns["check"](stub.fsp_layout_check(bad.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 2, 2))
+    assert stub.fsp_attn_bwd_workspace_bytes(1000, 8, 128) == lib.fsp_attn_bwd_workspace_bytes(1000, 8, 128)
 
 
 def test_forward_schedule_pairs_for_head_dim_128(lib):

@@ -216,7 +216,9 @@ def test_attention_golden_vectors():
     dq, dk, dv = ops.attn_bwd(q, k, v, o, do, lse, sched)
     torch.cuda.synchronize()
     assert (o.float().cpu() - torch.from_numpy(z["o"])).abs().max() <= 2e-2
-    assert (lse.cpu() - torch.from_numpy(z["lse"])).abs().max() <= 1e-3 * 10
+    ref_lse = torch.from_numpy(z["lse"])
+    # LSE: relative 1e-3 as stated in DESIGN.md §6 (absolute 1e-3 where |lse| < 1)
+    assert ((lse.cpu() - ref_lse).abs() / ref_lse.abs().clamp(min=1.0)).max() <= 1e-3
     for got, key in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
         torch.testing.assert_close(got.float().cpu(), torch.from_numpy(z[key]), atol=5e-2, rtol=5e-2)
 

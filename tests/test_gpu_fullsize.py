@@ -18,7 +18,7 @@ import numpy as np
 import pytest
 import torch
 
-from oracle.sampled_ref import key_rows, query_rows
+from sampled_check import check_sequence, sample_rows
 
 pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
@@ -26,24 +26,13 @@ GOLDEN = Path(__file__).resolve().parent / "golden"
 
 def _check_sequence(q, k, v, do, o, dq, dk, dv, lse, rows, kv_rows, tag):
     """All arguments [s, D] for one (sequence, head) (lse [s]); o/dq/dk/dv from the GPU."""
-    ref = query_rows(q, k, v, do, rows)
-    o_g = o.float().cpu().numpy()
-    np.testing.assert_allclose(o_g[rows], ref["o"], atol=2e-2, err_msg=f"{tag} O")
-    lse_g = lse.float().cpu().numpy()
-    np.testing.assert_allclose(lse_g[rows], ref["lse"], atol=2e-3, rtol=1e-3, err_msg=f"{tag} LSE")
-    np.testing.assert_allclose(dq.float().cpu().numpy()[rows], ref["dq"], atol=5e-2, rtol=5e-2,
-                               err_msg=f"{tag} dQ")
-    delta = (o.float() * do.float()).sum(-1).cpu().numpy()
-    kr = key_rows(q, k, v, do, kv_rows, lse_g, delta)
-    np.testing.assert_allclose(dk.float().cpu().numpy()[kv_rows], kr["dk"], atol=5e-2, rtol=5e-2,
-                               err_msg=f"{tag} dK")
-    np.testing.assert_allclose(dv.float().cpu().numpy()[kv_rows], kr["dv"], atol=5e-2, rtol=5e-2,
-                               err_msg=f"{tag} dV")
+    res = check_sequence(q, k, v, do, o[rows], dq[rows], dk[kv_rows], dv[kv_rows], o, lse, rows,
+                         kv_rows, tag)
+    assert res["ok"], res
 
 
 def _rows(s, rng, n=12):
-    pick = {0, 1, s // 2, s - 2, s - 1} | set(rng.integers(0, s, size=n).tolist())
-    return sorted(r for r in pick if 0 <= r < s)
+    return sample_rows(s, rng, n)
 
 
 def test_c2_full_step_sampled_rows():

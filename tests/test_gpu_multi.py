@@ -1,8 +1,15 @@
-"""Multi-GPU parity of the SP step over real NVSwitch peer memory (skipped on 1 GPU).
+"""Multi-rank parity of the SP step: real NVSwitch peer memory when the box has the GPUs,
+virtual ranks on one GPU otherwise (never skipped).
 
-Runs scripts/mgpu_parity.py under torchrun on 2 (and 4 when present) GPUs with plans
-produced by the reference planner, and checks the reassembled O / dQKV against the
-single-process CPU oracle."""
+* N GPUs present: scripts/mgpu_parity.py under torchrun (one process per GPU, symmetric
+  memory), reassembled O / dQKV against the single-process CPU oracle.
+* fewer GPUs: tests/vrank_parity.py runs the same plan with N virtual ranks on cuda:0 —
+  every rank its own executor, stream and heap, the same exchange / fused-epilogue /
+  barrier kernels (vranks.VirtualCluster) — against the same oracle.
+* BASELINE-size plans (C2 at N=4 FlexSP [2,1,1] and static SP=8; C4 at N=8 FlexSP with a
+  384K-token sequence, 52 heads split 7,7,7,7,6,6,6,6 at d=8) always run on virtual
+  ranks, checked through sampled rows (float64 oracle/sampled_ref.py).
+"""
 import os
 import subprocess
 import sys
@@ -16,22 +23,51 @@ ROOT = Path(__file__).resolve().parent.parent
 CASES = [(2, "c1_flexsp_2tier.json", 8, 128), (2, "c1_static2.json", 8, 128),
          (4, "rand0_n4_flexsp.json", 8, 128), (4, "rand2_n4_flexsp.json", 8, 128),
          (8, "rand1_n8_flexsp.json", 8, 128),
-         # uneven head splits: 5 heads over 2 ranks, 10 over 4
+         # uneven head splits: 5 heads over 2 ranks, 10 over 4, 13 over 8
          (2, "c1_static2.json", 5, 128), (4, "rand0_n4_flexsp.json", 10, 128),
+         (8, "rand1_n8_flexsp.json", 13, 128),
          # ranks left idle by a micro-batch (sum of degrees < N)
          (4, "idle_n4.json", 8, 128),
          # BASELINE configs[0] shape: C1 plan, 4 heads of 64 (h = 256)
          (2, "c1_flexsp_2tier.json", 4, 64)]
+VIRTUAL_ONLY = [
+    # a 9-token sequence at d = 8 (members holding only pad rows) and empty selected groups
+    (8, "tiny_n8.json", 8, 128),
+    (8, "rand1_n8_flexsp.json", 4, 64)]
+FULLSIZE = [(4, "c2_n4_flexsp.json", 32, 128), (8, "c2_n8_static.json", 32, 128),
+            (8, "c4_n8_flexsp.json", 52, 128)]
+
+
+def _run(cmd, timeout, env_extra=None):
+    env = dict(os.environ, OMP_NUM_THREADS="4", FSP_BARRIER_TIMEOUT_S="120")
+    env.update(env_extra or {})
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert '"ok": true' in res.stdout
+    return res.stdout
+
+
+def _virtual(mode, n, plan, heads, head_dim, timeout=900):
+    return _run([sys.executable, str(ROOT / "tests" / "vrank_parity.py"), mode, plan, str(n),
+                 str(heads), str(head_dim)], timeout, {"CUDA_DEVICE_MAX_CONNECTIONS": "32"})
 
 
 @pytest.mark.parametrize("n,plan,heads,head_dim", CASES)
 def test_mgpu_step_matches_oracle(n, plan, heads, head_dim):
-    if torch.cuda.device_count() < n:
-        pytest.skip(f"needs {n} GPUs")
-    env = dict(os.environ, OMP_NUM_THREADS="4")
+    if torch.cuda.device_count() < n:  # one-GPU box: the same plan on n virtual ranks
+        _virtual("dense", n, plan, heads, head_dim)
+        return
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + n),
            str(ROOT / "scripts" / "mgpu_parity.py"), plan, str(heads), str(head_dim)]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
-    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
-    assert '"ok": true' in res.stdout
+    _run(cmd, 600)
+
+
+@pytest.mark.parametrize("n,plan,heads,head_dim", VIRTUAL_ONLY)
+def test_virtual_ranks_match_oracle(n, plan, heads, head_dim):
+    _virtual("dense", n, plan, heads, head_dim)
+
+
+@pytest.mark.parametrize("n,plan,heads,head_dim", FULLSIZE)
+def test_virtual_ranks_fullsize_sampled(n, plan, heads, head_dim):
+    _virtual("sampled", n, plan, heads, head_dim, timeout=1800)

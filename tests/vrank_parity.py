@@ -1,0 +1,234 @@
+"""Multi-rank parity of the SP step on ONE GPU through virtual ranks (vranks.VirtualCluster).
+
+    python tests/vrank_parity.py dense   PLAN WORLD HEADS HEAD_DIM
+    python tests/vrank_parity.py sampled PLAN WORLD HEADS HEAD_DIM
+
+Runs a reference-planner plan for WORLD GPUs with WORLD virtual ranks — each its own
+FlexSPExecutor, CUDA stream and heap; the real fused-pack exchange kernels, attention with
+the fused head->seq epilogue, and the spinning group barriers between the streams — and
+checks the reassembled loader-order O and dQKV:
+
+* dense:   every row against the single-process CPU oracle (no SP; oracle/attention_ref.py)
+           after three repeated steps (heap reuse), plus the autograd Function
+           (FlexSPAttention) against the executor step bit for bit (O, dK, dV);
+* sampled: BASELINE-size plans (C2 259K tokens / C4 733K tokens with a 384K sequence and
+           52 heads split 7,7,7,7,6,6,6,6 at d=8) through sampled rows of one long and one
+           short sequence of every group against oracle/sampled_ref.py (float64).
+
+Launched as a subprocess by tests/test_gpu_multi.py (CUDA_DEVICE_MAX_CONNECTIONS has to
+be set before CUDA initialises; the barrier timeout turns an issue bug into a fault).
+Test infrastructure: only tests/ run it.
+"""
+import json
+import os
+import sys
+from pathlib import Path
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ.setdefault("FSP_BARRIER_TIMEOUT_S", "60")
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+from oracle.attention_ref import attention_bwd_ref, attention_fwd_ref  # noqa: E402
+from paper_2412_01523_b200 import ops  # noqa: E402
+from paper_2412_01523_b200.attention import FlexSPAttention  # noqa: E402
+from paper_2412_01523_b200.layout import head_split  # noqa: E402
+from paper_2412_01523_b200.vranks import VirtualCluster  # noqa: E402
+from sampled_check import check_sequence, sample_rows  # noqa: E402
+
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def load_plan(name):
+    p = GOLDEN / name
+    if p.exists():
+        return json.loads(p.read_text())
+    if name == "tiny_n8.json":
+        # a 9-token sequence at d = 8 (members 5..7 hold only pad rows), an empty selected
+        # group, and a d = 4 group beside two d = 2 groups
+        lengths = [9, 300, 40, 3, 129, 1]
+        return {"schema": 1, "strategy": "flexsp", "lengths": lengths, "micro_batches": [
+            {"selected_groups": [{"slot_id": 0, "degree": 8, "sequence_indices": [0]}]},
+            {"selected_groups": [{"slot_id": 1, "degree": 4, "sequence_indices": [1, 3]},
+                                 {"slot_id": 3, "degree": 2, "sequence_indices": [2, 5]},
+                                 {"slot_id": 4, "degree": 2, "sequence_indices": []}]},
+            {"selected_groups": [{"slot_id": 3, "degree": 2, "sequence_indices": [4]},
+                                 {"slot_id": 5, "degree": 2, "sequence_indices": []}]}]}
+    raise FileNotFoundError(name)
+
+
+def dense(plan_name, world, H, D):
+    plan = load_plan(plan_name)
+    lengths = plan["lengths"]
+    vc = VirtualCluster(world, H, D, "cuda")
+    sps = vc.prepare(plan, lengths)
+    T = sum(lengths)
+    g = torch.Generator().manual_seed(2024)
+    qkv = torch.randn(T, 3, H, D, generator=g).bfloat16()
+    dout = torch.randn(T, H, D, generator=g).bfloat16()
+    ins = [[qkv[torch.from_numpy(mb.local_tokens)].cuda() for mb in sp.micro_batches] for sp in sps]
+    dos = [[dout[torch.from_numpy(mb.local_tokens)].cuda() for mb in sp.micro_batches] for sp in sps]
+    got = {}
+
+    def sink(r, m, out, dqkv):  # stays on the device (no host sync while ranks issue)
+        if out is not None:
+            got[(r, m)] = (out.clone(), dqkv.clone())
+
+    for _ in range(3):  # repeated steps: heap reuse across steps and regrouping
+        got.clear()
+        vc.step(sps, ins, dos, sink=sink)
+    torch.cuda.synchronize()
+    # the autograd Function, all forwards before any backward, on every virtual rank
+    leaves, outs = {}, {}
+
+    def autograd_rank(r, ex):
+        for m in range(len(sps[r].micro_batches)):
+            leaves[(r, m)] = ins[r][m].clone().requires_grad_(True)
+            outs[(r, m)] = FlexSPAttention.apply(leaves[(r, m)], ex, sps[r], m)
+        for m in reversed(range(len(sps[r].micro_batches))):
+            outs[(r, m)].backward(dos[r][m])
+
+    vc.run(autograd_rank)
+    torch.cuda.synchronize()
+    autograd_ok = True
+    for key, (out, dqkv) in got.items():
+        gq = leaves[key].grad
+        autograd_ok = autograd_ok and torch.equal(outs[key].detach(), out) and \
+            torch.equal(gq[:, 1:], dqkv[:, 1:]) and \
+            bool(torch.allclose(gq[:, 0].float(), dqkv[:, 0].float(), atol=1e-2, rtol=1e-2))
+    o = torch.full((T, H, D), float("nan"))
+    dq = torch.full((T, 3, H, D), float("nan"))
+    for (r, m), (out, dqkv) in got.items():
+        t = torch.from_numpy(sps[r].micro_batches[m].local_tokens)
+        o[t] = out.float().cpu()
+        dq[t] = dqkv.float().cpu()
+    cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32)
+    o_ref, _ = attention_fwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], cu)
+    refs = attention_bwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], dout, cu)
+    e_o = (o - o_ref).abs()
+    ok = autograd_ok and bool(torch.isfinite(o).all()) and e_o.max() <= 2e-2 and e_o.mean() <= 2e-3
+    errs = []
+    for i, r in enumerate(refs):
+        e = (dq[:, i] - r).abs()
+        errs.append(float(e.max()))
+        cos = torch.nn.functional.cosine_similarity(dq[:, i].reshape(1, -1), r.reshape(1, -1)).item() \
+            if T else 1.0
+        ok = ok and bool(torch.isfinite(dq[:, i]).all()) and \
+            bool(torch.allclose(dq[:, i], r, atol=5e-2, rtol=5e-2)) and cos >= 0.999
+    degs = [sorted((gg["degree"] for gg in mb["selected_groups"]), reverse=True)
+            for mb in plan["micro_batches"]]
+    return {"mode": "dense", "plan": plan_name, "world": world, "heads": H, "head_dim": D,
+            "groups": degs, "tokens": T, "o_max": float(e_o.max()), "o_mean": float(e_o.mean()),
+            "grad_max": errs, "autograd_ok": autograd_ok, "ok": bool(ok)}
+
+
+def sampled(plan_name, world, H, D):
+    """BASELINE-size plans: inputs generated per sequence on the device, sampled rows
+    checked in float64 (oracle/sampled_ref.py via tests/sampled_check.py)."""
+    plan = load_plan(plan_name)
+    lengths = plan["lengths"]
+    offs = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    vc = VirtualCluster(world, H, D, "cuda")
+    sps = vc.prepare(plan, lengths)
+    hb8 = head_split(H, min(8, H))
+    heads = sorted({0, hb8[len(hb8) // 2], H - 1})
+    # sequences to check: in every group of every micro-batch its longest and shortest
+    checked = set()
+    for mb in plan["micro_batches"]:
+        for grp in mb["selected_groups"]:
+            idx = list(grp["sequence_indices"])
+            if idx:
+                checked.add(max(idx, key=lambda k: lengths[k]))
+                checked.add(min(idx, key=lambda k: lengths[k]))
+    # per-rank loader-order inputs, filled sequence by sequence
+    ins = [[torch.empty((mb.n_local, 3, H, D), dtype=torch.bfloat16, device="cuda")
+            for mb in sp.micro_batches] for sp in sps]
+    dos = [[torch.empty((mb.n_local, H, D), dtype=torch.bfloat16, device="cuda")
+            for mb in sp.micro_batches] for sp in sps]
+    keep = {}
+    g = torch.Generator(device="cuda")
+    for k, s in enumerate(lengths):
+        g.manual_seed(7000 + k)
+        x = torch.randn((s, 4, H, D), generator=g, device="cuda", dtype=torch.bfloat16)
+        lo, hi = int(offs[k]), int(offs[k + 1])
+        for r, sp in enumerate(sps):
+            for m, mb in enumerate(sp.micro_batches):
+                a, b = np.searchsorted(mb.local_tokens, [lo, hi])
+                if b > a:
+                    t0 = int(mb.local_tokens[a]) - lo
+                    assert int(mb.local_tokens[b - 1]) - lo == t0 + (b - a) - 1  # contiguous
+                    ins[r][m][a:b] = x[t0:t0 + (b - a), :3]
+                    dos[r][m][a:b] = x[t0:t0 + (b - a), 3]
+        if k in checked:
+            keep[k] = x[:, :, heads].contiguous()  # [s, 4, len(heads), D]
+        del x
+    rng = np.random.default_rng(0)
+    rows = {k: (sample_rows(lengths[k], rng), sample_rows(lengths[k], rng)) for k in checked}
+    # per (rank, micro-batch): local rows holding sampled tokens of checked sequences
+    want = {}
+    for r, sp in enumerate(sps):
+        for m, mb in enumerate(sp.micro_batches):
+            sel = []
+            for k in checked:
+                for i in sorted(set(rows[k][0]) | set(rows[k][1])):
+                    t = int(offs[k]) + i
+                    p = int(np.searchsorted(mb.local_tokens, t))
+                    if p < mb.n_local and int(mb.local_tokens[p]) == t:
+                        sel.append((p, t))
+            if sel:
+                want[(r, m)] = (torch.tensor([p for p, _ in sel], device="cuda"),
+                                np.array([t for _, t in sel]))
+    got = {}
+
+    def sink(r, m, out, dqkv):
+        if (r, m) in want:
+            idx = want[(r, m)][0]
+            got[(r, m)] = (out.index_select(0, idx), dqkv.index_select(0, idx))
+
+    vc.step(sps, ins, dos, sink=sink)
+    torch.cuda.synchronize()
+    o_at, d_at = {}, {}
+    for key, (o, d) in got.items():
+        for n, t in enumerate(want[key][1]):
+            o_at[int(t)] = o[n]
+            d_at[int(t)] = d[n]
+    del ins, dos
+    torch.cuda.synchronize()
+    report = []
+    for k in sorted(checked):
+        s = lengths[k]
+        qr, kr = rows[k]
+        x = keep[k]
+        for hi, h in enumerate(heads):
+            q, kk, v, do = (x[:, i, hi].contiguous() for i in range(4))
+            sched = ops.AttnSchedule.build(np.array([0, s], np.int32), "cuda", 1, head_dim=D)
+            o1, lse1 = ops.attn_fwd(q.view(s, 1, D), kk.view(s, 1, D), v.view(s, 1, D), sched)
+            o_rows = torch.stack([o_at[int(offs[k]) + i][h] for i in qr])
+            dq_rows = torch.stack([d_at[int(offs[k]) + i][0, h] for i in qr])
+            dk_rows = torch.stack([d_at[int(offs[k]) + i][1, h] for i in kr])
+            dv_rows = torch.stack([d_at[int(offs[k]) + i][2, h] for i in kr])
+            err = check_sequence(q, kk, v, do, o_rows, dq_rows, dk_rows, dv_rows, o1[:, 0],
+                                 lse1[0], qr, kr, f"seq {k} (len {s}) head {h}")
+            report.append({"seq": k, "len": s, "head": h, **err})
+    degs = [sorted((gg["degree"] for gg in mb["selected_groups"]), reverse=True)
+            for mb in plan["micro_batches"]]
+    return {"mode": "sampled", "plan": plan_name, "world": world, "heads": H, "head_dim": D,
+            "groups": degs, "tokens": int(offs[-1]), "checked": report,
+            "ok": all(r["ok"] for r in report)}
+
+
+def main():
+    mode, plan, world, H, D = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), \
+        int(sys.argv[5])
+    res = (dense if mode == "dense" else sampled)(plan, world, H, D)
+    print(json.dumps(res), flush=True)
+    sys.exit(0 if res["ok"] else 1)
+
+
+if __name__ == "__main__":
+    main()
