@@ -431,7 +431,14 @@ __global__ void __launch_bounds__(256) attn_bwd_post_kernel(const float* __restr
 #endif
 constexpr int kV2Compute = FSP_BWD_COMPUTE_WARPS;  // 8 or 16: 2 or 4 warps per lane quadrant
 constexpr int kV2Cols = 64 / (kV2Compute / 4);      // query columns per compute warp
-static_assert(kV2Compute == 8 || kV2Compute == 16, "2 or 4 compute warps per TMEM lane quadrant");
+// 4, 8 or 16 compute warps: 1, 2 or 4 per TMEM lane quadrant, each owning kV2Cols = 64, 32
+// or 16 query columns of a unit.  (Round 1 tried 4 warps while the TMEM loads / stores below
+// were written for 16 / 32 columns only and the softmax statistics were fetched by compute
+// threads 128..255 — with 4 warps 48 of the 64 S / dP columns were never loaded, 3/4 of P
+// and dS never stored and delta never fetched: the parity failure it saw.  Those paths are
+// now generic in kV2Cols and in the compute-thread count.)
+static_assert(kV2Compute == 4 || kV2Compute == 8 || kV2Compute == 16,
+              "1, 2 or 4 compute warps per TMEM lane quadrant");
 #ifndef FSP_BWD_REDUCE_WARPS
 #define FSP_BWD_REDUCE_WARPS 4
 #endif
@@ -778,13 +785,13 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     const int head = T.head, seq_start = T.seq_start, seqlen = T.seqlen, kt = T.kt,
               kv0 = T.kv0, n_it = T.n_it;
     const int kv_pos = kv0 + r;
-    // statistics of query tile `it`: thread ctid < 128 owns lse row ctid, others delta
-    auto load_stat = [&](int it) -> float {
-      const int t = ctid & 127;
+    // statistics entry e of query tile `it`: e < 128 is lse row e, e >= 128 delta row e-128
+    auto load_stat = [&](int e, int it) -> float {
+      const int t = e & 127;
       const int q0 = (kt + it) * kTile;
       const bool valid = q0 + t < seqlen;
       const int64_t gi = (int64_t)head * p.total_rows + seq_start + q0 + t;
-      if (ctid < 128) return valid ? -p.lse[gi] * kLog2e : -INFINITY;  // stored negated
+      if (e < 128) return valid ? -p.lse[gi] * kLog2e : -INFINITY;  // stored negated
       return valid ? p.delta[gi] : 0.f;
     };
     auto half = [&](auto diag_c, int it, int h) {
@@ -808,12 +815,16 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         return;
       }
       uint32_t sr[kV2Cols], dr[kV2Cols];
-      if (kV2Cols == 32) {
-        tmem_ld32(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(sr));
-        tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(dr));
+      const uint32_t col0 = h * 64 + ch * kV2Cols;
+      if (kV2Cols >= 32) {
+#pragma unroll
+        for (int c = 0; c < kV2Cols; c += 32) {
+          tmem_ld32(tmem + lane_addr + kV2ColS + col0 + c, *reinterpret_cast<uint32_t(*)[32]>(sr + c));
+          tmem_ld32(tmem + lane_addr + kV2ColDP + col0 + c, *reinterpret_cast<uint32_t(*)[32]>(dr + c));
+        }
       } else {
-        tmem_ld16(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, *reinterpret_cast<uint32_t(*)[16]>(sr));
-        tmem_ld16(tmem + lane_addr + kV2ColDP + h * 64 + ch * 16, *reinterpret_cast<uint32_t(*)[16]>(dr));
+        tmem_ld16(tmem + lane_addr + kV2ColS + col0, *reinterpret_cast<uint32_t(*)[16]>(sr));
+        tmem_ld16(tmem + lane_addr + kV2ColDP + col0, *reinterpret_cast<uint32_t(*)[16]>(dr));
       }
       tmem_ld_wait();
       uint32_t pk[kV2Cols / 2], dk[kV2Cols / 2];
@@ -839,11 +850,14 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         dk[i / 2] = pack_bf16(d0, d1);
       }
       // own S columns: P^T (bf16 pairs) in the first half, dS^T in the second (FSP_BWD_DS_TMEM)
-      if (kV2Cols == 32) {
-        tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 32, *reinterpret_cast<const uint32_t(*)[16]>(pk));
-        if (FSP_BWD_DS_TMEM)
-          tmem_st16(tmem + lane_addr + kV2ColS + h * 64 + ch * 32 + 16,
-                    *reinterpret_cast<const uint32_t(*)[16]>(dk));
+      if (kV2Cols >= 32) {
+#pragma unroll
+        for (int c = 0; c < kV2Cols / 2; c += 16) {
+          tmem_st16(tmem + lane_addr + kV2ColS + col0 + c, *reinterpret_cast<const uint32_t(*)[16]>(pk + c));
+          if (FSP_BWD_DS_TMEM)
+            tmem_st16(tmem + lane_addr + kV2ColS + col0 + kV2Cols / 2 + c,
+                      *reinterpret_cast<const uint32_t(*)[16]>(dk + c));
+        }
       } else {
         tmem_st8(tmem + lane_addr + kV2ColS + h * 64 + ch * 16, *reinterpret_cast<const uint32_t(*)[8]>(pk));
         if (FSP_BWD_DS_TMEM)
@@ -867,12 +881,21 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       if (cw == 0 && lane == 0) atomicAdd(&g_bwd_wait[10], (unsigned long long)(clock64() - tq0));
 #endif
     };
-    const bool stat_thread = ctid < 256;
-    float stat = (n_it > 0 && stat_thread) ? load_stat(0) : 0.f;
+    // 256 statistics per query tile (128 lse, 128 delta): stat entry e = ctid + j * threads
+    constexpr int kCT = 32 * kV2Compute;
+    constexpr int kStatPer = (256 + kCT - 1) / kCT;
+    float stat[kStatPer];
+#pragma unroll
+    for (int j = 0; j < kStatPer; ++j)
+      stat[j] = (n_it > 0 && ctid + j * kCT < 256) ? load_stat(ctid + j * kCT, 0) : 0.f;
     for (int it = 0; it < n_it; ++it) {
-      if (stat_thread) {
-        (ctid < 128 ? lse_s : delta_s)[((IT0 + it) & 1) * 128 + (ctid & 127)] = stat;
-        if (it + 1 < n_it) stat = load_stat(it + 1);  // latency hidden behind this tile
+#pragma unroll
+      for (int j = 0; j < kStatPer; ++j) {
+        const int e = ctid + j * kCT;
+        if (e < 256) {
+          (e < 128 ? lse_s : delta_s)[((IT0 + it) & 1) * 128 + (e & 127)] = stat[j];
+          if (it + 1 < n_it) stat[j] = load_stat(e, it + 1);  // latency hidden behind this tile
+        }
       }
       named_bar_sync(1, 32 * kV2Compute);
       if (it == 0) {

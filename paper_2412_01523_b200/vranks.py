@@ -18,6 +18,11 @@ This is how a one-GPU box checks the degree >= 2 path of plans for 2/4/8 GPUs
 * enough hardware queues for one stream per rank: set CUDA_DEVICE_MAX_CONNECTIONS >= 16
   before CUDA initialises (tests run the harness in a subprocess for that reason), so a
   spinning barrier never sits in front of another rank's work in a shared queue;
+* eager module loading (CUDA_MODULE_LOADING=EAGER before CUDA initialises): with lazy
+  loading, the first launch of a kernel loads its module and that load waits for the
+  kernels already running in the context — a spinning barrier of rank 0 then blocks the
+  host before it has issued rank 1's arrival (observed: rank 0 timed out waiting for
+  member 1 at its first barrier);
 * FSP_BARRIER_TIMEOUT_S bounds every barrier spin: an issue bug becomes a device fault
   with a message, not a hang.
 """
@@ -58,6 +63,9 @@ class VirtualCluster:
             raise RuntimeError(
                 f"VirtualCluster({world}) needs CUDA_DEVICE_MAX_CONNECTIONS >= {world + 1} "
                 "set before CUDA initialises (one hardware queue per virtual rank)")
+        if os.environ.get("CUDA_MODULE_LOADING", "LAZY").upper() != "EAGER":
+            raise RuntimeError("VirtualCluster needs CUDA_MODULE_LOADING=EAGER set before CUDA "
+                               "initialises (a lazy module load waits for the spinning barriers)")
         self.world = world
         self.device = torch.device(device)
         self.ptrs = [0] * world

@@ -49,7 +49,8 @@ def _run(cmd, timeout, env_extra=None):
 
 def _virtual(mode, n, plan, heads, head_dim, timeout=900):
     return _run([sys.executable, str(ROOT / "tests" / "vrank_parity.py"), mode, plan, str(n),
-                 str(heads), str(head_dim)], timeout, {"CUDA_DEVICE_MAX_CONNECTIONS": "32"})
+                 str(heads), str(head_dim)], timeout, {"CUDA_DEVICE_MAX_CONNECTIONS": "32",
+                                  "CUDA_MODULE_LOADING": "EAGER"})
 
 
 @pytest.mark.parametrize("n,plan,heads,head_dim", CASES)

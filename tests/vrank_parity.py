@@ -25,6 +25,7 @@ import sys
 from pathlib import Path
 
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 os.environ.setdefault("FSP_BARRIER_TIMEOUT_S", "60")
 
 import numpy as np  # noqa: E402
