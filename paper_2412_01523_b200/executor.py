@@ -128,6 +128,10 @@ class FlexSPExecutor:
         self.group = group
         self.heap: PeerHeap | None = None
         self.epoch = 0
+        # forward / backward calls so far: their parity picks the output slot, identically
+        # on every rank (every rank calls both for every micro-batch, idle ranks included)
+        self._n_fwd = 0
+        self._n_bwd = 0
         self._ws: dict[str, torch.Tensor] = {}
         self.timer = EventTimer()
         # Eq. (4) fused into the attention epilogues (O in the forward, dQ/dK/dV in the
@@ -190,8 +194,13 @@ class FlexSPExecutor:
                     max_local = max(max_local, int((g.shard(jj) >= 0).sum()))
         off = {}
         cur = _SIGNAL_BYTES
-        for name, elems in (("qkv_recv", 3 * max_recv), ("out_local", max_local * hd),
-                            ("do_recv", max_recv), ("dqkv_local", 3 * max_local * hd)):
+        # out_local / dqkv_local alternate between two slots (micro-batch parity), so a
+        # micro-batch's results can be read out (step_from_host's D2H copy) while the next
+        # micro-batch computes into the other slot
+        for name, elems in (("qkv_recv", 3 * max_recv), ("out_local0", max_local * hd),
+                            ("out_local1", max_local * hd), ("do_recv", max_recv),
+                            ("dqkv_local0", 3 * max_local * hd),
+                            ("dqkv_local1", 3 * max_local * hd)):
             off[name] = cur
             cur += _align(max(elems, 1) * 2)
         strategy = plan["strategy"] if isinstance(plan, dict) else getattr(plan, "strategy", "")
@@ -206,6 +215,7 @@ class FlexSPExecutor:
         self.heap = (self.heap_factory(nbytes) if self.heap_factory is not None else
                      PeerHeap(nbytes, self.device, self.world_size, self.group))
         self.epoch = 0
+        self._n_fwd = self._n_bwd = 0
 
     def _workspace(self, name: str, numel: int, dtype: torch.dtype) -> torch.Tensor:
         t = self._ws.get(name)
@@ -229,11 +239,18 @@ class FlexSPExecutor:
         return self.epoch
 
     # ------------------------------------------------------------ one micro-batch
+    def _out_off(self, sp: StepPlan) -> int:
+        return sp.offsets[f"out_local{self._n_fwd & 1}"]   # slot of the current forward
+
+    def _dqkv_off(self, sp: StepPlan) -> int:
+        return sp.offsets[f"dqkv_local{self._n_bwd & 1}"]  # slot of the current backward
+
     def local_buffers(self, sp: StepPlan, mb: RankMicroBatch):
-        """Views of this rank's output buffers for micro-batch `mb` (inside the heap)."""
-        out = self.heap.view(sp.offsets["out_local"], (mb.n_local, self.n_heads, self.head_dim),
+        """Views of this rank's output buffers (inside the heap) for the micro-batch whose
+        forward / backward is the current one."""
+        out = self.heap.view(self._out_off(sp), (mb.n_local, self.n_heads, self.head_dim),
                              torch.bfloat16)
-        dqkv = self.heap.view(sp.offsets["dqkv_local"], (mb.n_local, 3, self.n_heads, self.head_dim),
+        dqkv = self.heap.view(self._dqkv_off(sp), (mb.n_local, 3, self.n_heads, self.head_dim),
                               torch.bfloat16)
         return out, dqkv
 
@@ -247,6 +264,7 @@ class FlexSPExecutor:
         # with what the previous micro-batch left there.  Ranks of other groups never touch
         # these heaps, and a degree-1 group touches none, so groups run decoupled.
         ep_entry = self._next_epoch()
+        self._n_fwd += 1
         grp = mb.group
         if grp is None:
             for _ in range(2):
@@ -282,7 +300,7 @@ class FlexSPExecutor:
         scatter = None
         if self.fuse_head2seq:  # Eq. (4) inside the attention epilogue
             scatter = ops.HeadScatter(d, R, hb[j], H * D, 0, mb.unpack_table,
-                                      [self.heap.peer(r, off["out_local"]) for r in ranks])
+                                      [self.heap.peer(r, self._out_off(sp)) for r in ranks])
         with self.timer.span("attn_fwd", mb.fwd_flops):
             _, lse = ops.attn_fwd(recv[:, 0, :hn], recv[:, 1, :hn], recv[:, 2, :hn], mb.sched,
                                   self.scale, out=o_heads[:, :hn], scatter=scatter)
@@ -292,7 +310,7 @@ class FlexSPExecutor:
             return out_local, (recv[:, :, :hn], o_heads[:, :hn], lse)
         with self.timer.span("a2a", sent_out):
             ops.a2a("head2seq", o_heads.view(T, hm * D),
-                    [self.heap.peer(r, off["out_local"]) for r in ranks], degree=d, rank=j,
+                    [self.heap.peer(r, self._out_off(sp)) for r in ranks], degree=d, rank=j,
                     rows_per_rank=R, n_mats=1, n_heads=H, head_dim=D, dst_stride=H * D,
                     index=mb.unpack_table, head_begin=hb)
             self._barrier(ranks, self._next_epoch())
@@ -310,6 +328,7 @@ class FlexSPExecutor:
     def micro_batch_backward(self, sp: StepPlan, mb: RankMicroBatch, saved, dout_local: torch.Tensor):
         """Backward of micro_batch_forward: dout_local [n_local, H, D] -> dqkv_local view."""
         ep_entry = self._next_epoch()  # group entry barrier, as in the forward
+        self._n_bwd += 1
         grp = mb.group
         if grp is None:
             for _ in range(2):
@@ -349,7 +368,7 @@ class FlexSPExecutor:
         if self.fuse_head2seq:  # Eq. (4) for dQ/dK/dV inside the backward's epilogues
             _, dqkv_local = self.local_buffers(sp, mb)
             scatter = ops.HeadScatter(d, R, hb[j], 3 * H * D, H * D, mb.unpack_table,
-                                      [self.heap.peer(r, off["dqkv_local"]) for r in ranks])
+                                      [self.heap.peer(r, self._dqkv_off(sp)) for r in ranks])
             with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
                 ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, do_recv[:, :hn], lse,
                              mb.sched, self.scale, dq_accum=dq_acc, delta=delta, scatter=scatter)
@@ -364,7 +383,7 @@ class FlexSPExecutor:
         _, dqkv_local = self.local_buffers(sp, mb)
         with self.timer.span("a2a", 3 * sent_out):
             ops.a2a("head2seq", dqkv_heads.view(T, 3 * hm * D),
-                    [self.heap.peer(r, off["dqkv_local"]) for r in ranks], degree=d, rank=j,
+                    [self.heap.peer(r, self._dqkv_off(sp)) for r in ranks], degree=d, rank=j,
                     rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * H * D,
                     index=mb.unpack_table, head_begin=hb)
             self._barrier(ranks, self._next_epoch())
@@ -381,9 +400,10 @@ class FlexSPExecutor:
                 sink(m, out, dqkv)
 
     def step_from_host(self, sp: StepPlan, host_qkv: Sequence[torch.Tensor],
-                       host_dout: Sequence[torch.Tensor], sink=None,
-                       prefetch_next: tuple | None = None) -> torch.Tensor:
-        """The same step fed straight from pinned host memory (the data-loader path).
+                       host_dout: Sequence[torch.Tensor], host_out: Sequence[torch.Tensor] | None = None,
+                       host_dqkv: Sequence[torch.Tensor] | None = None, sink=None,
+                       prefetch_next: tuple | None = None) -> None:
+        """The same step fed from and returned to pinned host memory (the data-loader path).
 
         Micro-batch m+1's q/k/v and dO are copied host->device on a side stream into the
         other half of a double buffer while micro-batch m computes, so PCIe transfer and
@@ -391,16 +411,23 @@ class FlexSPExecutor:
         also starts the NEXT step's first micro-batch copy while this step's last
         micro-batch computes (what a data loader does between steps); the next call with
         those same host tensors then finds it in flight instead of copying again.
-        Returns a device fp32 scalar, the step's <O, dO> "loss" (a cheap reduction over
-        every output, read back by the caller).
+        With `host_out` / `host_dqkv` (pinned, [n_local, H, D] / [n_local, 3, H, D] per
+        micro-batch) each micro-batch's O and dQKV are copied device->host on a third
+        stream while the next micro-batch computes (PCIe is full duplex; the output
+        regions alternate between two heap slots, and a slot is rewritten only after its
+        copy-out finished).  The copies are in flight when this returns:
+        `d2h_stream` orders after them.
         """
         cur = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_h2d_stream"):
             self._h2d_stream = torch.cuda.Stream(self.device)
+            self.d2h_stream = torch.cuda.Stream(self.device)
             # persistent across calls: a copy must not overwrite a slot the previous step
             # is still reading (waiting on a never-recorded event is a no-op)
             self._h2d_consumed = [torch.cuda.Event() for _ in range(2)]
             self._h2d_loaded = [torch.cuda.Event() for _ in range(2)]
+            self._out_read = [torch.cuda.Event() for _ in range(2)]   # out_local slot copied out
+            self._dqkv_read = [torch.cuda.Event() for _ in range(2)]  # dqkv_local slot copied out
             self._h2d_slot = 0            # slot the next copy goes to (strictly alternating)
             self._h2d_prefetched = None   # (host qkv, host dout, slot) of an in-flight copy
         side = self._h2d_stream
@@ -417,7 +444,6 @@ class FlexSPExecutor:
             cur.wait_stream(side)
         bufs = [(self._workspace(f"h2d_qkv{k}", rows_needed * 3 * hd, torch.bfloat16),
                  self._workspace(f"h2d_do{k}", rows_needed * hd, torch.bfloat16)) for k in range(2)]
-        loss = torch.zeros((), dtype=torch.float32, device=self.device)
 
         def issue_copy(hq, hdo, rows) -> int:
             k = self._h2d_slot
@@ -452,11 +478,20 @@ class FlexSPExecutor:
             rows = mb.n_local
             q = bufs[k][0][:rows * 3 * hd].view(rows, 3, self.n_heads, self.head_dim)
             d = bufs[k][1][:rows * hd].view(rows, self.n_heads, self.head_dim)
+            # the output slots this micro-batch writes must have been copied out already
+            cur.wait_event(self._out_read[(self._n_fwd + 1) & 1])
             out, saved = self.micro_batch_forward(sp, mb, q)
+            cur.wait_event(self._dqkv_read[(self._n_bwd + 1) & 1])
             dqkv = self.micro_batch_backward(sp, mb, saved, d)
-            if out is not None and rows:
-                loss += torch.dot(out.reshape(-1).float(), d.reshape(-1).float())
             if sink is not None:
                 sink(m, out, dqkv)
             consumed[k].record(cur)
-        return loss
+            if host_out is not None and out is not None and rows:
+                so, sd = self._n_fwd & 1, self._n_bwd & 1
+                self.d2h_stream.wait_stream(cur)
+                with torch.cuda.stream(self.d2h_stream):
+                    host_out[m].view(rows, hd).copy_(out.reshape(rows, hd), non_blocking=True)
+                    host_dqkv[m].view(rows, 3 * hd).copy_(dqkv.reshape(rows, 3 * hd),
+                                                         non_blocking=True)
+                    self._out_read[so].record(self.d2h_stream)
+                    self._dqkv_read[sd].record(self.d2h_stream)
