@@ -442,8 +442,17 @@ static_assert(kV2Compute == 4 || kV2Compute == 8 || kV2Compute == 16,
 #ifndef FSP_BWD_REDUCE_WARPS
 #define FSP_BWD_REDUCE_WARPS 4
 #endif
+#ifndef FSP_BWD_REDUCE_SPLIT
+#define FSP_BWD_REDUCE_SPLIT 0  // with 8 reduction warps: 0 = split a unit's 64 columns,
+                                // 1 = split units by parity (each warp drains whole units)
+#endif
+#ifndef FSP_BWD_POLY_EVERY
+#define FSP_BWD_POLY_EVERY 0  // one exponential pair in N on the FMA pipe (ex2_poly2); 0 = none
+#endif
 constexpr int kV2Reduce = FSP_BWD_REDUCE_WARPS;  // 4 or 8: 1 or 2 warps per lane quadrant
-constexpr int kV2RedCols = 64 / (kV2Reduce / 4);   // dQ^T columns (query rows) per warp
+constexpr bool kRedSplitUnits = FSP_BWD_REDUCE_SPLIT && kV2Reduce == 8;
+constexpr int kV2RedCols = kRedSplitUnits ? 64 : 64 / (kV2Reduce / 4);  // dQ^T columns per warp
+constexpr int kTmFreeCount = kRedSplitUnits ? 4 : kV2Reduce;  // warps draining one unit
 constexpr int kV2Threads = 64 + 32 * (kV2Compute + kV2Reduce);
 constexpr uint32_t kV2ColS = 256, kV2ColDP = 384;
 
@@ -588,7 +597,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       mbar_init(s_full + i, 1);
       mbar_init(p_ready + i, kV2Compute);
       mbar_init(dq_full + i, 1);
-      mbar_init(tm_free + i, kV2Reduce);
+      mbar_init(tm_free + i, kTmFreeCount);
       mbar_init(ering.full + i, 1);
       mbar_init(ering.empty + i, kBwdRingConsumers);
     }
@@ -835,9 +844,15 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       for (int i = 0; i < kV2Cols; i += 2) {
         const uint64_t x2 =
             ffma2(f2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sl2x2, nls2[i / 2]);
-        float x0, x1;
-        f2_split(x2, x0, x1);
-        float p0 = ex2(x0), p1 = ex2(x1);
+        float p0, p1;
+        if (FSP_BWD_POLY_EVERY > 0 && (i / 2) % FSP_BWD_POLY_EVERY == FSP_BWD_POLY_EVERY - 1) {
+          ex2_poly2(x2, p0, p1);  // this pair on the FMA pipe, the rest on MUFU
+        } else {
+          float x0, x1;
+          f2_split(x2, x0, x1);
+          p0 = ex2(x0);
+          p1 = ex2(x1);
+        }
         if (kDiag) {  // causal on the diagonal tile: query column c0+i >= kv row r
           if (c0 + i < r) p0 = 0.f;
           if (c0 + i + 1 < r) p1 = 0.f;
@@ -1004,6 +1019,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     for (int u = 0; u < n_u; ++u) {
       const int it = u >> 1, h = u & 1;
       const uint32_t IT = (U0 + u) >> 1;
+      // unit-parity split: warp group `part` drains the units of stage h == part only, so
+      // one group's TMEM readout of unit U never queues behind the other's reductions of U-1
+      if (kRedSplitUnits && (int)((U0 + u) & 1) != part) continue;
 #if FSP_BWD_TIMING
       const long long tr0 = clock64();
 #endif
@@ -1024,7 +1042,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
 #pragma unroll
         for (int i = 0; i < kV2RedCols; ++i) qr[i] = 0u;
       } else {
-        tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + part * kV2RedCols,
+        tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + (kRedSplitUnits ? 0 : part * kV2RedCols),
                   *reinterpret_cast<uint32_t(*)[32]>(qr));
         if (kV2RedCols == 64)
           tmem_ld32(tmem + lane_addr + kV2ColDP + h * 64 + 32,
@@ -1035,7 +1053,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(tm_free + h);
       // first query row of this warp's columns (in sequence)
-      const int qb = (kt + it) * kTile + h * 64 + part * kV2RedCols;
+      const int qb = (kt + it) * kTile + h * 64 + (kRedSplitUnits ? 0 : part * kV2RedCols);
       float* base = head_base + (int64_t)qb * D;
       const int nvalid = seqlen - qb;
       if (FSP_BWD_ABLATE & 32) {  // profiling ablation: read dQ^T out of TMEM, drop it
