@@ -223,10 +223,47 @@ def sampled(plan_name, world, H, D):
             "ok": all(r["ok"] for r in report)}
 
 
+def stress(plan_name, world, H, D, repeats=12):
+    """Barrier / heap-reuse stress: the same plan stepped `repeats` times on virtual ranks
+    (every step regroups the ranks and reuses every heap region and signal slot); O, dK
+    and dV must come out bit-identical every time (dQ: its fp32 atomics make the order
+    free, within 1e-2), and the first step must match the dense oracle."""
+    res = dense(plan_name, world, H, D)
+    plan = load_plan(plan_name)
+    lengths = plan["lengths"]
+    vc = VirtualCluster(world, H, D, "cuda")
+    sps = vc.prepare(plan, lengths)
+    T = sum(lengths)
+    g = torch.Generator().manual_seed(99)
+    qkv = torch.randn(T, 3, H, D, generator=g).bfloat16()
+    dout = torch.randn(T, H, D, generator=g).bfloat16()
+    ins = [[qkv[torch.from_numpy(mb.local_tokens)].cuda() for mb in sp.micro_batches] for sp in sps]
+    dos = [[dout[torch.from_numpy(mb.local_tokens)].cuda() for mb in sp.micro_batches] for sp in sps]
+    runs = []
+    for _ in range(repeats):
+        got = {}
+        vc.step(sps, ins, dos, sink=lambda r, m, o, d, got=got: got.__setitem__(
+            (r, m), (o.clone(), d.clone())) if o is not None else None)
+        runs.append(got)
+    torch.cuda.synchronize()
+    same = True
+    worst_dq = 0.0
+    for got in runs[1:]:
+        for key, (o, d) in got.items():
+            o0, d0 = runs[0][key]
+            same = same and torch.equal(o, o0) and torch.equal(d[:, 1:], d0[:, 1:])
+            if d.numel():
+                worst_dq = max(worst_dq, float((d[:, 0].float() - d0[:, 0].float()).abs().max()))
+    res.update({"mode": "stress", "repeats": repeats, "bit_identical_o_dk_dv": bool(same),
+                "dq_max_run_to_run": worst_dq})
+    res["ok"] = bool(res["ok"] and same and worst_dq <= 1e-2)
+    return res
+
+
 def main():
     mode, plan, world, H, D = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), \
         int(sys.argv[5])
-    res = (dense if mode == "dense" else sampled)(plan, world, H, D)
+    res = {"dense": dense, "sampled": sampled, "stress": stress}[mode](plan, world, H, D)
     print(json.dumps(res), flush=True)
     sys.exit(0 if res["ok"] else 1)
 
