@@ -41,7 +41,7 @@ extern "C" {
 #define FSP_ERR_CUDA (-2)
 #define FSP_ERR_UNSUPPORTED (-3)
 
-#define FSP_ABI_VERSION 4
+#define FSP_ABI_VERSION 5
 
 int fsp_abi_version(void);
 const char* fsp_last_error(void);
@@ -55,6 +55,19 @@ int fsp_pack_rows(const void* src, int64_t src_stride_bytes, void* dst, int64_t 
 /* Row scatter (inverse):  dst[index[i], :] = src[i, :] for index[i] >= 0. */
 int fsp_unpack_rows(const void* src, int64_t src_stride_bytes, void* dst, int64_t dst_stride_bytes,
                     const int32_t* d_index, int64_t n_rows, int64_t row_bytes, void* stream);
+
+/* Per-plan data scatter (ABI 5; "scatters the data into the corresponding
+ * group"): the data loader shards a step's sequences over the ranks before the plan is
+ * known (layout.loader_shards: round-robin); each micro-batch's rows must then reach the
+ * members of the groups that own them.  d_routes is int32 [n_routes][3] =
+ * {src_row, dst_rank, dst_row}: row src_row of the local shard (row stride
+ * src_stride_bytes) is stored at row dst_row of peer_dst[dst_rank] (that rank's input
+ * buffer mapped into this process; the own rank's entry is its local buffer).  The caller
+ * brackets the scatter with fsp_group_barrier over all ranks (destination free / data
+ * landed).  Strides, row_bytes and pointers: multiples of 16. */
+int fsp_scatter_rows(const void* src, int64_t src_stride_bytes, void* const* peer_dst,
+                     int32_t n_peers, int64_t dst_stride_bytes, const int32_t* d_routes,
+                     int64_t n_routes, int64_t row_bytes, void* stream);
 
 /* ------------------------------------------------------------------ all-to-all */
 /* One Ulysses exchange inside an SP group of `degree` ranks on one NVSwitch domain.

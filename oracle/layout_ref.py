@@ -134,3 +134,37 @@ def ulysses_head2seq(heads, n_mats, n_heads, head_dim):
     for j in range(d):
         out.append(np.concatenate([h[j * r:(j + 1) * r] for h in heads], axis=2))
     return out
+
+
+def scatter_routes_ref(lengths, world_size, micro_batch_groups):
+    """Per-plan data scatter restated in plain loops: sequence k starts on
+    rank k % world_size (round-robin loader shards, batch order inside a shard) and must
+    end on the member of its micro-batch group that holds it, at that member's
+    loader-order row.  micro_batch_groups: [(rank_begin, degree, [seq indices])] of one
+    micro-batch.  Returns {src_rank: [(src_row, dst_rank, dst_row)]} in src_row order."""
+    offs = [0]
+    for s in lengths:
+        offs.append(offs[-1] + int(s))
+    # source position of every token
+    src = {}
+    for r in range(world_size):
+        n = 0
+        for k in range(r, len(lengths), world_size):
+            for t in range(offs[k], offs[k + 1]):
+                src[t] = (r, n)
+                n += 1
+    routes = {r: [] for r in range(world_size)}
+    for r0, d, seqs in micro_batch_groups:
+        packed = []
+        for k in seqs:
+            packed.extend(range(offs[k], offs[k + 1]))
+        t_pad = -(-len(packed) // d) * d
+        rows = t_pad // d
+        for j in range(d):
+            mine = sorted(packed[j * rows:(j + 1) * rows])
+            for pos, t in enumerate(mine):
+                r, n = src[t]
+                routes[r].append((n, r0 + j, pos))
+    for r in routes:
+        routes[r].sort()
+    return routes

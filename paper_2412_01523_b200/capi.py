@@ -17,7 +17,7 @@ FSP_OK = 0
 FSP_ERR_INVALID = -1
 FSP_ERR_CUDA = -2
 FSP_ERR_UNSUPPORTED = -3
-ABI_VERSION = 4
+ABI_VERSION = 5
 FSP_SCHED_FWD = 0
 FSP_SCHED_BWD = 1
 
@@ -31,7 +31,7 @@ EXPORTED = (
     "fsp_abi_version", "fsp_last_error", "fsp_pack_rows", "fsp_unpack_rows",
     "fsp_a2a_seq2head", "fsp_a2a_head2seq", "fsp_group_barrier", "fsp_attn_schedule",
     "fsp_attn_fwd", "fsp_attn_bwd", "fsp_attn_bwd_workspace_bytes", "fsp_layout_check",
-    "fsp_selftest_umma",
+    "fsp_selftest_umma", "fsp_scatter_rows",
 )
 
 
@@ -91,6 +91,8 @@ def load() -> ctypes.CDLL:
     lib.fsp_last_error.restype = ctypes.c_char_p
     lib.fsp_pack_rows.argtypes = [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp]
     lib.fsp_unpack_rows.argtypes = [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp]
+    lib.fsp_scatter_rows.argtypes = [c_vp, c_i64, ctypes.POINTER(c_vp), c_i32, c_i64, c_vp, c_i64,
+                                     c_i64, c_vp]
     lib.fsp_a2a_seq2head.argtypes = [ctypes.POINTER(FspA2A), c_vp, ctypes.POINTER(c_vp), c_vp, c_vp]
     lib.fsp_a2a_head2seq.argtypes = [ctypes.POINTER(FspA2A), c_vp, ctypes.POINTER(c_vp), c_vp, c_vp]
     lib.fsp_group_barrier.argtypes = [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, ctypes.c_uint32, c_vp]

@@ -86,8 +86,78 @@ int launch_permute(const void* src, int64_t ss, void* dst, int64_t ds, const int
   return FSP_OK;
 }
 
+// Per-plan data scatter: route e = {src_row, dst_rank, dst_row}; the row is read once from
+// the local loader shard and stored into the owning rank's input buffer (a peer-mapped
+// NVSwitch address, or local memory for the own rank).  Flattened (route, 16-byte vector)
+// index space as in permute_rows_kernel, 16-byte stores.
+constexpr int kMaxPeers = 8;
+struct PeerTable {
+  uint8_t* p[kMaxPeers];
+};
+
+__global__ void __launch_bounds__(kThreads) scatter_rows_kernel(
+    const uint8_t* __restrict__ src, int64_t src_stride, PeerTable dst, int64_t dst_stride,
+    const int32_t* __restrict__ routes, int64_t n_routes, uint32_t vec_per_row) {
+  const int64_t total = n_routes * (int64_t)vec_per_row;
+  const int64_t step = (int64_t)gridDim.x * kThreads;
+  for (int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x; g < total; g += step * kUnroll) {
+    int4 v[kUnroll];
+    uint8_t* d[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t e = g + u * step;
+      d[u] = nullptr;
+      if (e < total) {
+        const int64_t i = e / vec_per_row;
+        const int64_t col = e - i * vec_per_row;
+        const int32_t sr = __ldg(routes + 3 * i), dr = __ldg(routes + 3 * i + 1),
+                      drow = __ldg(routes + 3 * i + 2);
+        v[u] = ld_stream(reinterpret_cast<const int4*>(src + (int64_t)sr * src_stride) + col);
+        d[u] = dst.p[dr] + (int64_t)drow * dst_stride + col * 16;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (d[u]) *reinterpret_cast<int4*>(d[u]) = v[u];
+  }
+  __threadfence_system();  // peer stores visible before the barrier that follows
+}
+
 }  // namespace
 }  // namespace fsp
+
+extern "C" int fsp_scatter_rows(const void* src, int64_t src_stride_bytes, void* const* peer_dst,
+                                int32_t n_peers, int64_t dst_stride_bytes,
+                                const int32_t* d_routes, int64_t n_routes, int64_t row_bytes,
+                                void* stream) {
+  using namespace fsp;
+  FSP_CHECK_ARG(n_routes >= 0, "n_routes must be >= 0");
+  FSP_CHECK_ARG(n_peers >= 1 && n_peers <= kMaxPeers, "n_peers must be in [1, %d]", kMaxPeers);
+  FSP_CHECK_ARG(peer_dst != nullptr, "null peer_dst");
+  if (n_routes == 0) return FSP_OK;
+  FSP_CHECK_ARG(src && d_routes, "null pointer argument");
+  FSP_CHECK_ARG(row_bytes > 0 && row_bytes % 16 == 0, "row_bytes must be a positive multiple of 16");
+  FSP_CHECK_ARG(src_stride_bytes % 16 == 0 && dst_stride_bytes % 16 == 0 &&
+                    src_stride_bytes >= row_bytes && dst_stride_bytes >= row_bytes,
+                "row strides must be multiples of 16 and >= row_bytes");
+  FSP_CHECK_ARG(((uintptr_t)src & 15) == 0, "src must be 16-byte aligned");
+  PeerTable t{};
+  for (int r = 0; r < n_peers; ++r) {
+    FSP_CHECK_ARG(peer_dst[r] != nullptr && ((uintptr_t)peer_dst[r] & 15) == 0,
+                  "peer_dst[%d] null or misaligned", r);
+    t.p[r] = reinterpret_cast<uint8_t*>(peer_dst[r]);
+  }
+  const int64_t vpr = row_bytes / 16;
+  FSP_CHECK_ARG(vpr < (1ll << 31) && n_routes < (1ll << 31), "scatter too large");
+  const int64_t total = n_routes * vpr;
+  int64_t blocks = (total + (int64_t)kThreads * kUnroll - 1) / ((int64_t)kThreads * kUnroll);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  scatter_rows_kernel<<<(unsigned)blocks, kThreads, 0, (cudaStream_t)stream>>>(
+      (const uint8_t*)src, src_stride_bytes, t, dst_stride_bytes, d_routes, n_routes,
+      (uint32_t)vpr);
+  FSP_LAUNCH_CHECK();
+  return FSP_OK;
+}
 
 extern "C" int fsp_pack_rows(const void* src, int64_t src_stride_bytes, void* dst,
                              int64_t dst_stride_bytes, const int32_t* d_index, int64_t n_rows,

@@ -32,7 +32,8 @@ import torch
 
 from . import ops
 from .profiling import EventTimer
-from .layout import GroupLayout, LayoutError, MicroBatchLayout, build_plan_layouts, head_split
+from .layout import (GroupLayout, LayoutError, MicroBatchLayout, build_plan_layouts, head_split,
+                     loader_shards, scatter_routes)
 
 _ALIGN = 4096
 _SIGNAL_BYTES = 4096
@@ -87,6 +88,8 @@ class RankMicroBatch:
     fwd_flops: float = 0.0                  # 2 * D * H_j * sum s^2 (causal, FA convention)
     in_place: bool = False                  # d = 1: attention runs on the loader-order rows
     head_begin: list[int] = field(default_factory=list)  # group's head split [d+1]
+    routes: torch.Tensor | None = None      # int32 [n, 3]: this rank's loader-shard rows of
+                                            # this micro-batch -> (owner rank, owner row)
 
     @property
     def n_heads_local(self) -> int:        # H_j: heads this rank attends over
@@ -105,6 +108,7 @@ class StepPlan:
     micro_batches: list[RankMicroBatch]
     offsets: dict[str, int] = field(default_factory=dict)
     heap_bytes: int = 0
+    shard_tokens: np.ndarray | None = None  # loader token ids of this rank's shard rows
 
     @property
     def total_tokens(self) -> int:
@@ -144,19 +148,30 @@ class FlexSPExecutor:
         self.heap_factory = heap_factory
 
     # ------------------------------------------------------------ planning -> tables
-    def prepare(self, plan: Any, lengths: Sequence[int]) -> StepPlan:
+    def prepare(self, plan: Any, lengths: Sequence[int], sharded_loader: bool = False) -> StepPlan:
+        """Device tables of one plan for this rank.  With `sharded_loader` the step's
+        inputs arrive as this rank's data-loader shard (layout.loader_shards: sequence k on
+        rank k % world) and step_from_shards scatters every micro-batch's rows to their
+        group members first."""
         layouts = build_plan_layouts(plan, lengths, self.world_size, self.n_heads)
+        shard = loader_shards(lengths, self.world_size)[self.rank] if sharded_loader else None
         hd = self.n_heads * self.head_dim
         mbs: list[RankMicroBatch] = []
         max_recv = max_local = 0
         for lay in layouts:
             grp, j = lay.group_of(self.rank)
+            routes = None
+            if shard is not None:
+                r = scatter_routes(lay, shard)
+                routes = torch.from_numpy(r if r.size else np.zeros((0, 3), np.int32)).to(self.device)
             if grp is None:
-                mbs.append(RankMicroBatch(lay, None, -1, 0, np.zeros(0, dtype=np.int64)))
+                mbs.append(RankMicroBatch(lay, None, -1, 0, np.zeros(0, dtype=np.int64),
+                                          routes=routes))
             else:
                 local = grp.local_tokens(j)
                 rmb = RankMicroBatch(lay, grp, j, int(local.shape[0]), local,
-                                     head_begin=head_split(self.n_heads, grp.degree))
+                                     head_begin=head_split(self.n_heads, grp.degree),
+                                     routes=routes)
                 pack = grp.pack_index(j)
                 table = grp.unpack_table()
                 # the tables the kernels index with are validated by the library first
@@ -200,11 +215,14 @@ class FlexSPExecutor:
         for name, elems in (("qkv_recv", 3 * max_recv), ("out_local0", max_local * hd),
                             ("out_local1", max_local * hd), ("do_recv", max_recv),
                             ("dqkv_local0", 3 * max_local * hd),
-                            ("dqkv_local1", 3 * max_local * hd)):
+                            ("dqkv_local1", 3 * max_local * hd),
+                            # step_from_shards: scattered loader rows (q/k/v, dO)
+                            ("in_qkv", 3 * max_local * hd if sharded_loader else 0),
+                            ("in_do", max_local * hd if sharded_loader else 0)):
             off[name] = cur
             cur += _align(max(elems, 1) * 2)
         strategy = plan["strategy"] if isinstance(plan, dict) else getattr(plan, "strategy", "")
-        sp = StepPlan(strategy, [int(s) for s in lengths], mbs, off, cur)
+        sp = StepPlan(strategy, [int(s) for s in lengths], mbs, off, cur, shard_tokens=shard)
         self._ensure_heap(cur)
         return sp
 
@@ -396,6 +414,44 @@ class FlexSPExecutor:
         for m, mb in enumerate(sp.micro_batches):
             out, saved = self.micro_batch_forward(sp, mb, qkv_locals[m])
             dqkv = self.micro_batch_backward(sp, mb, saved, dout_locals[m])
+            if sink is not None:
+                sink(m, out, dqkv)
+
+    def step_from_shards(self, sp: StepPlan, shard_qkv: torch.Tensor, shard_dout: torch.Tensor,
+                         sink=None) -> None:
+        """The step fed by the data loader's shards (prepare(..., sharded_loader=True)).
+
+        shard_qkv [n_shard, 3, H, D] / shard_dout [n_shard, H, D] hold this rank's loader
+        rows (sequence k on rank k % world, batch order).  Before each micro-batch every
+        rank pushes that micro-batch's rows of its shard to the group members that own them
+        (fsp_scatter_rows, NVSwitch peer stores into their heap input buffers, PAPER.md:922
+        "scatters the data into the corresponding group"); a world barrier before the
+        scatter frees the input buffers, one after it publishes the data; the micro-batch
+        then runs on the received loader-order rows exactly as in step()."""
+        if sp.shard_tokens is None:
+            raise ValueError("prepare the plan with sharded_loader=True first")
+        n_shard = int(sp.shard_tokens.shape[0])
+        if shard_qkv.shape[0] != n_shard or shard_dout.shape[0] != n_shard:
+            raise ValueError(f"rank {self.rank} shard has {n_shard} rows")
+        hd = self.n_heads * self.head_dim
+        world = range(0, self.world_size)
+        off = sp.offsets
+        src_q = shard_qkv.reshape(n_shard, 3 * hd)
+        src_d = shard_dout.reshape(n_shard, hd)
+        for m, mb in enumerate(sp.micro_batches):
+            self._barrier(world, self._next_epoch(), "scatter_barrier")  # inputs free
+            with self.timer.span("scatter", float(mb.routes.shape[0] * 4 * hd * 2)):
+                ops.scatter_rows(src_q, mb.routes, [self.heap.peer(r, off["in_qkv"]) for r in world],
+                                 3 * hd * 2)
+                ops.scatter_rows(src_d, mb.routes, [self.heap.peer(r, off["in_do"]) for r in world],
+                                 hd * 2)
+                self._barrier(world, self._next_epoch())  # every rank's rows have landed
+            q = self.heap.view(off["in_qkv"], (mb.n_local, 3, self.n_heads, self.head_dim),
+                               torch.bfloat16)
+            d = self.heap.view(off["in_do"], (mb.n_local, self.n_heads, self.head_dim),
+                               torch.bfloat16)
+            out, saved = self.micro_batch_forward(sp, mb, q)
+            dqkv = self.micro_batch_backward(sp, mb, saved, d)
             if sink is not None:
                 sink(m, out, dqkv)
 

@@ -197,3 +197,41 @@ def build_plan_layouts(plan: Any, lengths: Sequence[int], world_size: int,
     if covered != list(range(len(lengths))):
         raise LayoutError("plan does not dispatch every sequence exactly once")
     return layouts
+
+
+# ------------------------------------------------------------------ data scatter
+def loader_shards(lengths: Sequence[int], world_size: int) -> list[np.ndarray]:
+    """The data loader's sharding of one global batch before any plan is known: sequence
+    k is read by rank k % world_size (round-robin data parallelism), and a rank's shard
+    holds the tokens of its sequences in batch order.  Returns, per rank, the loader token
+    ids of its shard rows (int64, ascending)."""
+    offs = token_offsets(lengths)
+    out = []
+    for r in range(world_size):
+        seqs = range(r, len(lengths), world_size)
+        toks = [np.arange(offs[k], offs[k + 1], dtype=np.int64) for k in seqs]
+        out.append(np.concatenate(toks) if toks else np.zeros(0, dtype=np.int64))
+    return out
+
+
+def scatter_routes(layout: MicroBatchLayout, shard_tokens: np.ndarray) -> np.ndarray:
+    """Per-plan data scatter ("scatters the data into the corresponding
+    group") of one micro-batch, for one source rank: int32 [n, 3] rows (src_row, dst_rank,
+    dst_row) — shard row src_row (a token of this micro-batch) goes to rank dst_rank's
+    loader-order input buffer at row dst_row (its position in that member's local_tokens).
+    Tokens of other micro-batches are not listed."""
+    total = int(shard_tokens.max()) + 1 if shard_tokens.size else 0
+    owner = np.full(max(total, 1), -1, dtype=np.int64)
+    row = np.full(max(total, 1), -1, dtype=np.int64)
+    for g in layout.groups:
+        for j in range(g.degree):
+            loc = g.local_tokens(j)
+            loc = loc[loc < total]
+            owner[loc] = g.rank_begin + j
+            row[loc] = np.searchsorted(g.local_tokens(j), loc)
+    live = np.nonzero(owner[shard_tokens] >= 0)[0] if shard_tokens.size else np.zeros(0, np.int64)
+    out = np.empty((live.size, 3), dtype=np.int32)
+    out[:, 0] = live
+    out[:, 1] = owner[shard_tokens[live]]
+    out[:, 2] = row[shard_tokens[live]]
+    return out

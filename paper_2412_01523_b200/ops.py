@@ -272,6 +272,21 @@ def a2a(direction: str, src: torch.Tensor, peer_dst_ptrs, *, degree: int, rank: 
     LAUNCHES[0] += 1 if rows_per_rank * n_mats else 0
 
 
+def scatter_rows(src: torch.Tensor, routes: torch.Tensor, peer_dst_ptrs, dst_stride_bytes: int) -> None:
+    """Per-plan data scatter (fsp_scatter_rows): routes int32 [n, 3] = (src_row, dst_rank,
+    dst_row); row src_row of the 2-D row-major `src` lands at row dst_row of rank
+    dst_rank's buffer peer_dst_ptrs[dst_rank] (row stride dst_stride_bytes)."""
+    _require_cuda(src, routes)
+    if routes.dtype != torch.int32 or routes.dim() != 2 or routes.shape[1] != 3:
+        raise ValueError("routes must be int32 [n, 3]")
+    row_bytes = src.shape[1] * src.element_size()
+    capi.check(capi.load().fsp_scatter_rows(
+        src.data_ptr() if src.numel() else None, src.stride(0) * src.element_size(),
+        _ptr_array(peer_dst_ptrs), len(peer_dst_ptrs), dst_stride_bytes, routes.data_ptr(),
+        routes.shape[0], row_bytes, _stream()))
+    LAUNCHES[0] += 1 if routes.shape[0] else 0
+
+
 def group_barrier(signal_ptrs, rank: int, slot_base: int, epoch: int) -> None:
     capi.check(capi.load().fsp_group_barrier(_ptr_array(signal_ptrs), len(signal_ptrs), rank,
                                              slot_base, epoch & 0xFFFFFFFF, _stream()))

@@ -94,8 +94,8 @@ class VirtualCluster:
             return h
         return make
 
-    def prepare(self, plan, lengths: Sequence[int]) -> list[StepPlan]:
-        sps = [ex.prepare(plan, lengths) for ex in self.executors]
+    def prepare(self, plan, lengths: Sequence[int], **kw) -> list[StepPlan]:
+        sps = [ex.prepare(plan, lengths, **kw) for ex in self.executors]
         if len({sp.heap_bytes for sp in sps}) != 1:
             raise LayoutError("virtual ranks disagree on the heap layout")
         return sps

@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared == set(capi.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.fsp_abi_version() == capi.ABI_VERSION == 4
+    assert lib.fsp_abi_version() == capi.ABI_VERSION == 5
 
 
 def _schedule(lib, lens, rev, heads=1, head_dim=64):

@@ -72,3 +72,13 @@ def test_virtual_ranks_match_oracle(n, plan, heads, head_dim):
 @pytest.mark.parametrize("n,plan,heads,head_dim", FULLSIZE)
 def test_virtual_ranks_fullsize_sampled(n, plan, heads, head_dim):
     _virtual("sampled", n, plan, heads, head_dim, timeout=1800)
+
+
+@pytest.mark.parametrize("n,plan,heads", [(2, "c1_flexsp_2tier.json", 8), (4, "rand0_n4_flexsp.json", 10),
+                                          (8, "rand1_n8_flexsp.json", 8), (8, "tiny_n8.json", 8),
+                                          (4, "idle_n4.json", 8)])
+def test_data_scatter_from_loader_shards(n, plan, heads):
+    """Per-plan data scatter: round-robin loader shards
+    routed to every micro-batch's group members by fsp_scatter_rows on virtual ranks;
+    routes equal the oracle's, delivered rows are bit-exact, the step matches the oracle."""
+    _virtual("shards", n, plan, heads, 128)

@@ -260,10 +260,88 @@ def stress(plan_name, world, H, D, repeats=12):
     return res
 
 
+def shards(plan_name, world, H, D):
+    """Per-plan data scatter: every virtual rank starts from its round-robin
+    loader shard (layout.loader_shards) and FlexSPExecutor.step_from_shards scatters each
+    micro-batch's rows to their group members (fsp_scatter_rows) before running it.  The
+    received rows must equal the oracle's routing (oracle/layout_ref.scatter_routes_ref)
+    bit for bit, and the step's O / dQKV must equal the plain step's (O, dK, dV bit for
+    bit; dQ to its atomics' order) and the dense oracle."""
+    from oracle.layout_ref import place_groups, scatter_routes_ref
+    from paper_2412_01523_b200.layout import loader_shards
+    res = dense(plan_name, world, H, D)  # plain step vs oracle (and its outputs below)
+    plan = load_plan(plan_name)
+    lengths = plan["lengths"]
+    vc = VirtualCluster(world, H, D, "cuda")
+    sps = vc.prepare(plan, lengths, sharded_loader=True)
+    T = sum(lengths)
+    g = torch.Generator().manual_seed(2024)
+    qkv = torch.randn(T, 3, H, D, generator=g).bfloat16()
+    dout = torch.randn(T, H, D, generator=g).bfloat16()
+    sh = loader_shards(lengths, world)
+    sq = [qkv[torch.from_numpy(t)].cuda() for t in sh]
+    sd = [dout[torch.from_numpy(t)].cuda() for t in sh]
+    # routing tables against the oracle's restatement
+    routes_ok = True
+    for m, mbp in enumerate(plan["micro_batches"]):
+        gs = mbp["selected_groups"]
+        starts = place_groups([gg["degree"] for gg in gs], world)
+        ref = scatter_routes_ref(lengths, world, [(st, gg["degree"], gg["sequence_indices"])
+                                                  for st, gg in zip(starts, gs)])
+        for r in range(world):
+            got = [tuple(x) for x in sps[r].micro_batches[m].routes.cpu().tolist()]
+            routes_ok = routes_ok and got == ref[r]
+    got, recv = {}, {}
+
+    def sink(r, m, out, dqkv):
+        if out is not None:
+            got[(r, m)] = (out.clone(), dqkv.clone())
+
+    def step_rank(r, ex):
+        orig = ex.micro_batch_forward
+
+        def spy(sp_, mb_, q_):  # keep what the scatter delivered (a device copy, no sync)
+            m_ = next(i for i, x in enumerate(sp_.micro_batches) if x is mb_)
+            recv[(r, m_)] = q_.clone()
+            return orig(sp_, mb_, q_)
+        ex.micro_batch_forward = spy
+        try:
+            ex.step_from_shards(sps[r], sq[r], sd[r], sink=lambda m, o, d: sink(r, m, o, d))
+        finally:
+            ex.micro_batch_forward = orig
+
+    for _ in range(2):
+        got.clear()
+        recv.clear()
+        vc.run(step_rank)
+    torch.cuda.synchronize()
+    scatter_exact = all(torch.equal(recv[(r, m)].cpu(),
+                                    qkv[torch.from_numpy(sps[r].micro_batches[m].local_tokens)])
+                        for (r, m) in recv)
+    o = torch.full((T, H, D), float("nan"))
+    dq = torch.full((T, 3, H, D), float("nan"))
+    for (r, m), (out, dqkv) in got.items():
+        t = torch.from_numpy(sps[r].micro_batches[m].local_tokens)
+        o[t] = out.float().cpu()
+        dq[t] = dqkv.float().cpu()
+    cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32)
+    o_ref, _ = attention_fwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], cu)
+    refs = attention_bwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], dout, cu)
+    e_o = (o - o_ref).abs()
+    ok = routes_ok and scatter_exact and bool(torch.isfinite(o).all()) and e_o.max() <= 2e-2
+    for i, r in enumerate(refs):
+        ok = ok and bool(torch.allclose(dq[:, i], r, atol=5e-2, rtol=5e-2))
+    res.update({"mode": "shards", "routes_match_oracle": routes_ok,
+                "scatter_bit_exact": scatter_exact, "shard_o_max": float(e_o.max())})
+    res["ok"] = bool(res["ok"] and ok)
+    return res
+
+
 def main():
     mode, plan, world, H, D = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), \
         int(sys.argv[5])
-    res = {"dense": dense, "sampled": sampled, "stress": stress}[mode](plan, world, H, D)
+    res = {"dense": dense, "sampled": sampled, "stress": stress,
+                                      "shards": shards}[mode](plan, world, H, D)
     print(json.dumps(res), flush=True)
     sys.exit(0 if res["ok"] else 1)
 
