@@ -1,16 +1,20 @@
 """C3 full training step (BASELINE.json configs[2]): GPT-13B-shape, 40 layers, fwd + bwd +
-gradient all-reduce + SGD, adaptive (FlexSP) vs static Ulysses SP, one process per GPU.
+optimizer, adaptive (FlexSP) vs static Ulysses SP, one process per GPU.
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/bench_full_step.py \
-        [--layers 40] [--steps 3] [--warmup 2] [--strategy both]
+        [--layers 40] [--steps 3] [--warmup 2] [--strategy both] [--replicated]
 
-Model: 40 x FlexSPTransformerLayer(hidden 5120, 40 heads, 4x MLP), bf16 weights replicated
-on every rank (FSDP/ZeRO is SURVEY §8f rank 4, out of scope), per-layer activation
+Model: 40 x FlexSPTransformerLayer(hidden 5120, 40 heads, 4x MLP), per-layer activation
 checkpointing (the layer inputs of the 252,160-token batch would not fit otherwise).
+Model state (default, "ZeRO with PyTorch FSDP" PAPER.md:917): ZeRO-3
+sharding over all ranks (paper_2412_01523_b200/zero.py) — per-layer flat bf16 parameter
+shards all-gathered before each layer (next layer prefetched on a communication stream),
+per-layer gradient buckets reduce-scattered as soon as the layer's backward completes,
+fp32 master shards with SGD-momentum (or --optimizer adamw).  --replicated: round 1's
+baseline — bf16 replicas, a NCCL all-reduce per parameter after the backward, plain SGD.
 One step = for every micro-batch of the plan: 40 layers forward on the rank's loader-order
 rows, synthetic loss <out, dy>, backward (recomputing each layer, attention through
-FlexSPAttention = the SP path of this repo); then a NCCL all-reduce of every gradient over
-all ranks and an SGD update.  Plans: tests/golden/c3_n{N}_{flexsp,static}.json (the
+FlexSPAttention = the SP path of this repo); then the optimizer update.  Plans: tests/golden/c3_n{N}_{flexsp,static}.json (the
 reference planner on the C3 batch).  Timing: CUDA events around the steps, max over ranks.
 Prints one JSON line per strategy on rank 0.  Needs >= 2 GPUs (weights + gradients +
 checkpoints exceed one GPU's 180 GB at 40 layers).
@@ -44,6 +48,9 @@ def main():
     ap.add_argument("--strategy", default="both", choices=["flexsp", "static", "both"])
     ap.add_argument("--config", default="c3full")
     ap.add_argument("--per-mb", action="store_true", help="split the SP-path spans per micro-batch")
+    ap.add_argument("--replicated", action="store_true",
+                    help="round-1 baseline: bf16 replicas + per-parameter all-reduce + SGD")
+    ap.add_argument("--optimizer", default="sgd", choices=["sgd", "adamw"])
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -55,6 +62,11 @@ def main():
     layers = [FlexSPTransformerLayer(HIDDEN, HEADS, device=dev, seed=1000 + i)
               for i in range(args.layers)]
     params = [p for l in layers for p in l.parameters()]
+    zs = None
+    if not args.replicated:
+        from paper_2412_01523_b200.zero import ZeroStack
+        zs = ZeroStack(layers, world, rank, optimizer=args.optimizer)
+        torch.cuda.empty_cache()
     ex = FlexSPExecutor(world, rank, HEADS, HIDDEN // HEADS, dev)
     strategies = ["flexsp", "static"] if args.strategy == "both" else [args.strategy]
     out = {}
@@ -70,12 +82,19 @@ def main():
         def step():
             for m in range(len(sp.micro_batches)):
                 ex.timer.tag = f"@mb{m}" if args.per_mb else ""
+                if zs is not None:
+                    zs.begin_micro_batch()
                 h = xs[m]
                 for layer in layers:
                     h = checkpoint(layer, h, ex, sp, m, use_reentrant=False)
                 loss = (h.float() * dys[m].float()).sum()
+                if zs is not None:
+                    zs.begin_backward()
                 if h.requires_grad:
                     loss.backward()
+            if zs is not None:  # reduce-scatters already ran during the backward
+                zs.step(1e-6)
+                return
             for p in params:  # data/sequence-parallel gradient sum (library collective)
                 if p.grad is None:
                     p.grad = torch.zeros_like(p)
@@ -122,8 +141,15 @@ def main():
                 "warmup": args.warmup, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": "C3: 40 x GPT-13B layer (h=5120, H=40, D=128, MLP 4h), "
                                        "gen_longtail(32, pareto(1.1, 1024), max 131072, seed 0) = "
-                                       "252,160 tokens; per-layer activation checkpointing; NCCL "
-                                       "gradient all-reduce + SGD (bf16 replicas; FSDP out of scope)"},
+                                       "252,160 tokens; per-layer activation checkpointing",
+                           "model_state": ("bf16 replicas, per-parameter NCCL all-reduce, SGD"
+                                           if zs is None else
+                                           f"ZeRO-3 over {world} ranks: per-layer all-gather "
+                                           "(prefetched) / reduce-scatter buckets, fp32 master "
+                                           f"shards, {args.optimizer}"),
+                           "model_state_bytes_per_rank": (None if zs is None else
+                                                          zs.sharded_bytes()["bytes_per_rank"]),
+                           "peak_mem_gb_rank0": torch.cuda.max_memory_allocated(dev) / 1e9},
                 "strategies": out}
         if "flexsp" in out and "static" in out:
             line["speedup_flexsp_over_static"] = out["static"]["ms_per_step"] / out["flexsp"]["ms_per_step"]
