@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--out", default=str(ROOT / "profiles" / "r01_calibration"))
     ap.add_argument("--per-degree", type=int, default=5)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--batches", default="c2,c3", help="golden batches the loads are drawn from")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -43,8 +44,11 @@ def main():
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/fsp_nccl.{os.getpid()}.log")
         dist.init_process_group("nccl", device_id=dev)
-    plan_doc = json.loads((ROOT / "tests" / "golden" / "c2_n1_flexsp.json").read_text())
-    lengths_all = plan_doc["lengths"]
+    # loads drawn from the C2 and C3 long-tail batches (1K .. 131K-token sequences), so the
+    # fit covers the lengths the planner actually deals out
+    lengths_all = []
+    for name in args.batches.split(","):
+        lengths_all += json.loads((ROOT / "tests" / "golden" / f"{name}_n1_flexsp.json").read_text())["lengths"]
     degrees = [d for d in (1, 2, 4, 8) if d <= world]
     loads = calibrate.group_loads(lengths_all, degrees, args.per_degree)
     ex = FlexSPExecutor(world, rank, H, D, dev)
@@ -71,7 +75,11 @@ def main():
         summ = ex.timer.summary()
         mine = {"comp": (summ.get("attn_fwd", {}).get("ms", 0.0) + summ.get("attn_bwd", {}).get("ms", 0.0))
                 / args.reps / 1e3,
-                "comm": summ.get("a2a", {}).get("ms", 0.0) / args.reps / 1e3}
+                # kernel-only exchange time: the a2a span minus the group barrier that
+                # closes it (the barrier holds the other members' compute skew, which the
+                # cost model's comm term does not describe)
+                "comm": max(0.0, summ.get("a2a", {}).get("ms", 0.0) -
+                            summ.get("group_barrier", {}).get("ms", 0.0)) / args.reps / 1e3}
         allr = [mine]
         if world > 1:
             allr = [None] * world
@@ -87,6 +95,7 @@ def main():
         try:
             fr, merged = calibrate.fit(rows, allow_underdetermined=len(degrees) < 2)
             pred = calibrate.predict(merged, rows)
+            result["per_degree"] = calibrate.per_degree_errors(merged, rows)
             result.update({"coefficients": merged.to_json_dict(),
                            "comp_rel_error": fr.comp_rel_error, "mem_rel_error": fr.mem_rel_error,
                            "comm_rel_error_d_ge_2": pred["comm_rel_error_d_ge_2"],
