@@ -32,13 +32,15 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
+    shards = "--shards" in sys.argv  # inputs from round-robin loader shards (step_from_shards)
+    sys.argv = [a for a in sys.argv if a != "--shards"]
     name = sys.argv[1] if len(sys.argv) > 1 else DEFAULT[world]
     plan = json.loads((ROOT / "tests" / "golden" / name).read_text())
     lengths = plan["lengths"]
     H = int(sys.argv[2]) if len(sys.argv) > 2 else 8  # H % d != 0: uneven head split
     D = int(sys.argv[3]) if len(sys.argv) > 3 else 128
     ex = FlexSPExecutor(world, rank, H, D, dev)
-    sp = ex.prepare(plan, lengths)
+    sp = ex.prepare(plan, lengths, sharded_loader=shards)
     T = sum(lengths)
     g = torch.Generator().manual_seed(2024)
     qkv = torch.randn(T, 3, H, D, generator=g).bfloat16()
@@ -52,9 +54,16 @@ def main():
             return
         got[m] = (sp.micro_batches[m].local_tokens, out.float().cpu(), dqkv.float().cpu())
 
+    if shards:  # the per-plan data scatter over NVSwitch
+        from paper_2412_01523_b200.layout import loader_shards
+        mine = torch.from_numpy(loader_shards(lengths, world)[rank])
+        sq, sd = qkv[mine].to(dev), dout[mine].to(dev)
     for rep in range(3):  # repeat: exercises heap reuse across steps and regrouping
         got.clear()
-        ex.step(sp, ins, dos, sink=sink)
+        if shards:
+            ex.step_from_shards(sp, sq, sd, sink=sink)
+        else:
+            ex.step(sp, ins, dos, sink=sink)
     torch.cuda.synchronize()
     # the same micro-batches through the autograd Function, all forwards before any
     # backward: outputs and dK/dV must equal the executor step's bit for bit on every rank
@@ -99,7 +108,7 @@ def main():
                 torch.allclose(dq[:, i], r, atol=5e-2, rtol=5e-2))
         degs = [sorted((gg["degree"] for gg in mb["selected_groups"]), reverse=True)
                 for mb in plan["micro_batches"]]
-        print(json.dumps({"plan": name, "world": world, "heads": H, "head_dim": D, "groups": degs, "tokens": T,
+        print(json.dumps({"plan": name, "world": world, "shards": shards, "heads": H, "head_dim": D, "groups": degs, "tokens": T,
                           "o_max": float(e_o.max()), "o_mean": float(e_o.mean()),
                           "grad_max": errs, "autograd_ok": autograd_ok, "ok": ok}), flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)

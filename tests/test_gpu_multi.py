@@ -81,4 +81,10 @@ def test_data_scatter_from_loader_shards(n, plan, heads):
     """Per-plan data scatter: round-robin loader shards
     routed to every micro-batch's group members by fsp_scatter_rows on virtual ranks;
     routes equal the oracle's, delivered rows are bit-exact, the step matches the oracle."""
+    if torch.cuda.device_count() >= n:  # the real NVSwitch scatter too
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+               str(29650 + n), str(ROOT / "scripts" / "mgpu_parity.py"), plan, str(heads), "128",
+               "--shards"]
+        _run(cmd, 600)
     _virtual("shards", n, plan, heads, 128)
