@@ -41,7 +41,10 @@ extern "C" {
 #define FSP_ERR_CUDA (-2)
 #define FSP_ERR_UNSUPPORTED (-3)
 
-#define FSP_ABI_VERSION 5
+#define FSP_ABI_VERSION 6
+
+/* FspAttnFwd / FspAttnBwd .flags */
+#define FSP_ATTN_NONCAUSAL 1
 
 int fsp_abi_version(void);
 const char* fsp_last_error(void);
@@ -170,6 +173,9 @@ typedef struct FspAttnFwd {
   int32_t head_dim;
   float softmax_scale;
   FspHeadScatter scatter; /* ABI 4: optional fused head->seq of O (degree 0 = off) */
+  int32_t flags;          /* ABI 6: FSP_ATTN_NONCAUSAL = every query row of a sequence sees
+                             every key row of it (a context-parallel block whose keys all
+                             precede its queries); 0 = causal */
 } FspAttnFwd;
 
 typedef struct FspAttnBwd {
@@ -195,6 +201,7 @@ typedef struct FspAttnBwd {
   int32_t head_dim;
   float softmax_scale;
   FspHeadScatter scatter; /* ABI 4: optional fused head->seq of dQ/dK/dV (degree 0 = off) */
+  int32_t flags;          /* ABI 6: FSP_ATTN_NONCAUSAL (as in FspAttnFwd) */
 } FspAttnBwd;
 
 /* CTA schedule: writes n entries of two int32 {seq << 16 | unit, head} to tiles_host

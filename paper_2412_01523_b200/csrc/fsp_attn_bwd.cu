@@ -53,6 +53,7 @@ struct BwdParams {
   float scale_log2;
   int32_t n_tiles;  // schedule entries (the persistent kernel walks them)
   ScatterDev sc;  // fused head->seq of dK / dV (matrices 1, 2); sc.degree == 0: off
+  int32_t noncausal;  // FSP_ATTN_NONCAUSAL (v2 kernel): every kv row meets every query row
 };
 
 template <int D>
@@ -492,6 +493,7 @@ __device__ unsigned int g_bwd_done;
 // One schedule entry of the backward: 128 kv rows (kv tile kt) of one sequence x head.
 struct KvTile {
   int head, seq_start, seqlen, kt, kv0, nq, n_it, n_u;
+  int qt0;  // first query tile this kv tile meets: kt (causal) or 0 (non-causal)
 };
 
 __device__ __forceinline__ KvTile decode_kv(const BwdParams& p, int w) {
@@ -504,7 +506,8 @@ __device__ __forceinline__ KvTile decode_kv(const BwdParams& p, int w) {
   t.seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
   t.kv0 = t.kt * kTile;
   t.nq = (t.seqlen + kTile - 1) / kTile;
-  t.n_it = t.nq - t.kt;
+  t.qt0 = p.noncausal ? 0 : t.kt;
+  t.n_it = t.nq - t.qt0;
   t.n_u = 2 * t.n_it;
   return t;
 }
@@ -642,7 +645,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
           const uint32_t item = 2 * U0 + li;
           const int slot = item % L::kSlots;
           const uint32_t ph = (item / L::kSlots) & 1;
-          const int row = T.seq_start + T.kv0 + (li >> 1) * 64;
+          const int row = T.seq_start + T.qt0 * kTile + (li >> 1) * 64;
           mbar_wait(ring_empty + slot, ph ^ 1);
           mbar_expect_tx(ring_full + slot, L::kHalfBytes);
           const CUtensorMap* map = (li & 1) ? &tm_do : &tm_q;
@@ -791,13 +794,16 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     const int w = bwd_take<kPersistent, true>(ering, k);
     if (w >= p.n_tiles) break;
     const KvTile T = decode_kv(p, w);
-    const int head = T.head, seq_start = T.seq_start, seqlen = T.seqlen, kt = T.kt,
+    const int head = T.head, seq_start = T.seq_start, seqlen = T.seqlen, qt0 = T.qt0,
               kv0 = T.kv0, n_it = T.n_it;
     const int kv_pos = kv0 + r;
+    // non-causal: key rows past the sequence end must not contribute (their K rows belong to
+    // the next sequence); causal masking covers them implicitly
+    const bool kv_dead = kv_pos >= seqlen;
     // statistics entry e of query tile `it`: e < 128 is lse row e, e >= 128 delta row e-128
     auto load_stat = [&](int e, int it) -> float {
       const int t = e & 127;
-      const int q0 = (kt + it) * kTile;
+      const int q0 = (qt0 + it) * kTile;
       const bool valid = q0 + t < seqlen;
       const int64_t gi = (int64_t)head * p.total_rows + seq_start + q0 + t;
       if (e < 128) return valid ? -p.lse[gi] * kLog2e : -INFINITY;  // stored negated
@@ -853,9 +859,13 @@ __global__ void __launch_bounds__(kV2Threads, 1)
           p0 = ex2(x0);
           p1 = ex2(x1);
         }
-        if (kDiag) {  // causal on the diagonal tile: query column c0+i >= kv row r
-          if (c0 + i < r) p0 = 0.f;
-          if (c0 + i + 1 < r) p1 = 0.f;
+        if (kDiag) {
+          if (p.noncausal) {  // the last, partial kv tile: rows past the sequence end
+            if (kv_dead) p0 = p1 = 0.f;
+          } else {  // causal on the diagonal tile: query column c0+i >= kv row r
+            if (c0 + i < r) p0 = 0.f;
+            if (c0 + i + 1 < r) p1 = 0.f;
+          }
         }
         const uint64_t ds2 = fmul2(
             f2(p0, p1), fsub2(f2(__uint_as_float(dr[i]), __uint_as_float(dr[i + 1])), dl2[i / 2]));
@@ -913,7 +923,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         }
       }
       named_bar_sync(1, 32 * kV2Compute);
-      if (it == 0) {
+      const bool masked = p.noncausal ? kv0 + kTile > seqlen : it == 0;
+      if (masked) {
         half(std::true_type{}, it, 0);
         half(std::true_type{}, it, 1);
       } else {
@@ -1014,7 +1025,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     const int w = bwd_take<kPersistent, true>(ering, k);
     if (w >= p.n_tiles) break;
     const KvTile T = decode_kv(p, w);
-    const int kt = T.kt, seqlen = T.seqlen, n_u = T.n_u;
+    const int qt0 = T.qt0, seqlen = T.seqlen, n_u = T.n_u;
     float* head_base = p.dq_accum + ((int64_t)T.head * p.total_rows + T.seq_start) * D + r;
     for (int u = 0; u < n_u; ++u) {
       const int it = u >> 1, h = u & 1;
@@ -1053,7 +1064,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(tm_free + h);
       // first query row of this warp's columns (in sequence)
-      const int qb = (kt + it) * kTile + h * 64 + (kRedSplitUnits ? 0 : part * kV2RedCols);
+      const int qb = (qt0 + it) * kTile + h * 64 + (kRedSplitUnits ? 0 : part * kV2RedCols);
       float* base = head_base + (int64_t)qb * D;
       const int nvalid = seqlen - qb;
       if (FSP_BWD_ABLATE & 32) {  // profiling ablation: read dQ^T out of TMEM, drop it
@@ -1128,6 +1139,7 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     p.sc = sc;
     const int64_t grid = a->n_tiles;
     p.n_tiles = a->n_tiles;
+    p.noncausal = (a->flags & FSP_ATTN_NONCAUSAL) ? 1 : 0;
     if (D == 128) {
       const int smem = BwdSmemV2::kBytes + 1024;
       // Persistent launch (CTAs steal not-yet-launched entries) unless the head->seq exchange
@@ -1174,6 +1186,9 @@ extern "C" int fsp_attn_bwd(const FspAttnBwd* a, void* stream) {
                 a->head_dim);
   FSP_CHECK_ARG(a->n_heads >= 1, "n_heads must be >= 1");
   FSP_CHECK_ARG(a->total_rows >= 0 && a->n_tiles >= 0, "negative sizes");
+  FSP_CHECK_ARG((a->flags & ~FSP_ATTN_NONCAUSAL) == 0, "unknown attention flags 0x%x", a->flags);
+  FSP_CHECK_ARG(!(a->flags & FSP_ATTN_NONCAUSAL) || a->head_dim == 128,
+                "FSP_ATTN_NONCAUSAL needs head_dim 128");
   if (a->total_rows == 0 && a->n_tiles == 0) return FSP_OK;  // empty group: no-op
   int rc = check_attn_common(a->q, a->k, a->v, a->q_stride, a->k_stride, a->v_stride,
                              a->d_cu_seqlens, a->d_tiles, a->n_tiles, a->n_seq, a->total_rows,

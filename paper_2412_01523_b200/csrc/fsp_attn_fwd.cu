@@ -39,6 +39,7 @@ struct FwdParams {
   float scale_log2;
   int32_t n_tiles;  // schedule entries (the persistent pair kernel walks them)
   ScatterDev sc;  // fused head->seq of O (sc.degree == 0: off)
+  int32_t noncausal;  // FSP_ATTN_NONCAUSAL: every query row sees every key row (pair kernel)
 };
 
 template <int D>
@@ -377,6 +378,13 @@ __device__ __forceinline__ PairTile decode_pair(const FwdParams& p, int w) {
   t.seqlen = p.cu_seqlens[seq + 1] - p.cu_seqlens[seq];
   t.q0 = pair * 256;
   t.has_b = t.q0 + 128 < t.seqlen;
+  if (p.noncausal) {  // every kv tile of the sequence, for both tiles
+    const int nkv = (t.seqlen + 127) / 128;
+    t.n_a = nkv;
+    t.n_b = t.has_b ? nkv : 0;
+    t.n_kv = nkv;
+    return t;
+  }
   t.n_a = 2 * pair + 1;                   // kv tiles seen by tile A (causal)
   t.n_b = t.has_b ? 2 * pair + 2 : 0;     // ... by tile B
   t.n_kv = t.has_b ? t.n_b : t.n_a;
@@ -718,7 +726,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       }
       // The diagonal tile (causal mask) and the interior tiles get separate straight-line
       // code: per-pair masking branches would serialise the MUFU / FFMA2 streams.
-      const int lim = q_pos - j * 128;  // causal: column c valid iff c <= lim (diagonal tile)
+      // column c of the last kv tile is valid iff c <= lim: causal, the diagonal tile
+      // (key row <= query row); non-causal, the sequence's last key row
+      const int lim = p.noncausal ? seqlen - 1 - j * 128 : q_pos - j * 128;
       auto tile_body = [&](auto diag_c) {
         constexpr bool kDiag = decltype(diag_c)::value;
         // pass 1: row max; four independent FMNMX3 chains over chunked TMEM loads (the
@@ -971,6 +981,7 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
   if ((rc = scatter_from_abi(a->scatter, 1, a->n_heads, D, a->total_rows, &p.sc))) return rc;
   p.n_tiles = a->n_tiles;
+  p.noncausal = (a->flags & FSP_ATTN_NONCAUSAL) ? 1 : 0;
   if (D == 128) {  // schedule entries are 256-row tile pairs (fsp_attn_schedule, head_dim 128)
     const int smem = Fwd2Smem::kBytes + 1024;
     // Persistent launch (CTAs steal not-yet-launched entries, so an entry's Q load and first
@@ -1074,6 +1085,9 @@ extern "C" int fsp_attn_fwd(const FspAttnFwd* a, void* stream) {
                 a->head_dim);
   FSP_CHECK_ARG(a->n_heads >= 1, "n_heads must be >= 1");
   FSP_CHECK_ARG(a->total_rows >= 0 && a->n_tiles >= 0, "negative sizes");
+  FSP_CHECK_ARG((a->flags & ~FSP_ATTN_NONCAUSAL) == 0, "unknown attention flags 0x%x", a->flags);
+  FSP_CHECK_ARG(!(a->flags & FSP_ATTN_NONCAUSAL) || a->head_dim == 128,
+                "FSP_ATTN_NONCAUSAL needs head_dim 128");
   if (a->total_rows == 0 && a->n_tiles == 0) return FSP_OK;
   int rc = check_attn_common(a->q, a->k, a->v, a->q_stride, a->k_stride, a->v_stride,
                              a->d_cu_seqlens, a->d_tiles, a->n_tiles, a->n_seq, a->total_rows,

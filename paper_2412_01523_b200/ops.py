@@ -57,6 +57,29 @@ def unpack_rows(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor) -> to
     return out
 
 
+def pack_rows_ptr(src_ptr: int, src_stride_bytes: int, index: torch.Tensor,
+                  out: torch.Tensor) -> torch.Tensor:
+    """pack_rows from a raw device address (e.g. a peer rank's heap mapped over NVSwitch)."""
+    _require_cuda(index, out)
+    row_bytes = out.shape[1] * out.element_size()
+    capi.check(capi.load().fsp_pack_rows(src_ptr, src_stride_bytes, out.data_ptr(),
+                                         out.stride(0) * out.element_size(), index.data_ptr(),
+                                         out.shape[0], row_bytes, _stream()))
+    LAUNCHES[0] += 1 if out.shape[0] else 0
+    return out
+
+
+def unpack_rows_ptr(src: torch.Tensor, index: torch.Tensor, dst_ptr: int,
+                    dst_stride_bytes: int) -> None:
+    """unpack_rows into a raw device address (e.g. a peer rank's heap)."""
+    _require_cuda(src, index)
+    row_bytes = src.shape[1] * src.element_size()
+    capi.check(capi.load().fsp_unpack_rows(src.data_ptr(), src.stride(0) * src.element_size(),
+                                           dst_ptr, dst_stride_bytes, index.data_ptr(),
+                                           src.shape[0], row_bytes, _stream()))
+    LAUNCHES[0] += 1 if src.shape[0] else 0
+
+
 # ---------------------------------------------------------------- attention schedule
 @dataclass
 class AttnSchedule:
@@ -152,10 +175,11 @@ def _rows_view_ok(t: torch.Tensor, H: int, D: int) -> None:
 
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSchedule,
              softmax_scale: float | None = None, out: torch.Tensor | None = None,
-             scatter: HeadScatter | None = None):
+             scatter: HeadScatter | None = None, causal: bool = True):
     """Varlen causal attention forward; q/k/v [T, H, D] bf16 (row-strided views OK).
     `scatter` fuses the head->seq exchange of O into the epilogue (O is still written
-    to `out`)."""
+    to `out`).  causal=False (FSP_ATTN_NONCAUSAL, D=128): every query row of a sequence
+    sees every key row of it — a context-parallel block whose keys precede its queries."""
     _require_cuda(q, k, v)
     T, H, D = q.shape
     for t in (q, k, v):
@@ -172,6 +196,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
                         sched.n_fwd, sched.n_seq, T, H, D, scale)
     if scatter is not None:
         a.scatter = scatter.to_c()
+    a.flags = 0 if causal else capi.FSP_ATTN_NONCAUSAL
     capi.check(capi.load().fsp_attn_fwd(ctypes.byref(a), _stream()))
     LAUNCHES[0] += 1 if sched.n_fwd else 0
     return o, lse
@@ -179,7 +204,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
 
 def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | None = None,
              dq=None, dk=None, dv=None, dq_accum=None, delta=None,
-             scatter: HeadScatter | None = None):
+             scatter: HeadScatter | None = None, causal: bool = True):
     """Varlen causal attention backward -> (dq, dk, dv), each [T, H, D] bf16.
 
     dq_accum (fp32 [H, T, D]) and delta (fp32 [H, T]) are optional reusable workspaces
@@ -220,6 +245,7 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
                         sched.n_bwd, sched.n_seq, T, H, D, scale)
     if scatter is not None:
         a.scatter = scatter.to_c()
+    a.flags = 0 if causal else capi.FSP_ATTN_NONCAUSAL
     capi.check(capi.load().fsp_attn_bwd(ctypes.byref(a), _stream()))
     LAUNCHES[0] += (2 if T else 0) + (1 if sched.n_bwd else 0)
     return dq, dk, dv

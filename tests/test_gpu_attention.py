@@ -239,3 +239,35 @@ def test_matches_flash_attn_varlen_on_c2_subset():
     for got, ref in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
         torch.testing.assert_close(got.float(), ref.float(), atol=5e-2, rtol=5e-2)
         assert _cos(got, ref) >= 0.999
+
+
+@pytest.mark.parametrize("lengths,H", [([128], 2), ([300, 1, 129], 2), ([1000, 777], 3)])
+def test_noncausal_matches_sdpa(lengths, H):
+    """FSP_ATTN_NONCAUSAL (ABI 6, the context-parallel cross blocks): every query row of a
+    sequence attends every key row of it — O, LSE, dQ, dK, dV against fp32 SDPA without a
+    mask, with separate q and k/v buffers as ring attention passes them."""
+    ops = _ops()
+    D = 128
+    cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32)
+    T = int(cu[-1])
+    g = torch.Generator().manual_seed(T + H)
+    q, k, v, do = (torch.randn(T, H, D, generator=g).bfloat16() for _ in range(4))
+    sched = ops.AttnSchedule.build(cu, "cuda", H, head_dim=D)
+    qd, kd, vd, dod = q.cuda(), k.cuda(), v.cuda(), do.cuda()
+    o, lse = ops.attn_fwd(qd, kd, vd, sched, causal=False)
+    dq, dk, dv = ops.attn_bwd(qd, kd, vd, o, dod, lse, sched, causal=False)
+    torch.cuda.synchronize()
+    for a, b in zip(cu[:-1], cu[1:]):
+        if b == a:
+            continue
+        qs, ks, vs = (t[a:b].float().transpose(0, 1).requires_grad_(True) for t in (q, k, v))
+        ref = torch.nn.functional.scaled_dot_product_attention(qs[None], ks[None], vs[None])[0]
+        ref.backward(do[a:b].float().transpose(0, 1))
+        ref_lse = torch.logsumexp((qs @ ks.transpose(1, 2)) / np.sqrt(D), dim=-1)
+        got_o = o[a:b].float().cpu().transpose(0, 1)
+        assert (got_o - ref.detach()).abs().max() <= 2e-2
+        rel = ((lse[:, a:b].cpu() - ref_lse.detach()).abs() / ref_lse.detach().abs().clamp(min=1)).max()
+        assert rel <= 1e-3
+        for got, t in ((dq, qs), (dk, ks), (dv, vs)):
+            torch.testing.assert_close(got[a:b].float().cpu().transpose(0, 1), t.grad,
+                                       atol=5e-2, rtol=5e-2)

@@ -88,3 +88,17 @@ def test_data_scatter_from_loader_shards(n, plan, heads):
                "--shards"]
         _run(cmd, 600)
     _virtual("shards", n, plan, heads, 128)
+
+
+@pytest.mark.parametrize("n,tokens,heads", [(2, 2048, 2), (4, 4096, 3), (8, 8192, 2), (4, 1000 * 8, 2)])
+def test_ring_attention_context_parallel(n, tokens, heads):
+    """Context parallelism (ring.RingAttention, zig-zag chunks, non-causal cross blocks
+    through FSP_ATTN_NONCAUSAL, peer-memory K/V fetches and dK/dV returns) on virtual ranks
+    against the dense fp32 oracle of the whole causal sequence (chunks of 1000 rows
+    exercise partial 128-row tiles)."""
+    if torch.cuda.device_count() >= n:  # over real NVSwitch peer memory too
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+               str(29670 + n), str(ROOT / "scripts" / "ring_parity.py"), str(tokens), str(heads)]
+        _run(cmd, 600)
+    _virtual("ring", n, str(tokens), heads, 128)

@@ -337,11 +337,71 @@ def shards(plan_name, world, H, D):
     return res
 
 
+def ring(plan_name, world, H, D):
+    """Context parallelism (ring.RingAttention) on `world` virtual ranks: one causal
+    sequence of `plan_name` tokens (an integer here) cut into 2*world zig-zag chunks;
+    the reassembled O / LSE / dQ / dK / dV must match the dense fp32 oracle."""
+    from paper_2412_01523_b200.ring import RingAttention, RingLayout, zigzag_rows
+    S = int(plan_name)
+    vc = VirtualCluster(world, H, D, "cuda")
+    rows = S // world
+    nbytes = RingLayout(rows, H, D).offsets(world)["end"]
+    for ex in vc.executors:
+        ex._ensure_heap(nbytes)
+    g = torch.Generator().manual_seed(11)
+    qkv = torch.randn(S, 3, H, D, generator=g).bfloat16()
+    dout = torch.randn(S, H, D, generator=g).bfloat16()
+    rings = [RingAttention(world, r, H, D, vc.heaps[r]) for r in range(world)]
+    idx = [torch.from_numpy(zigzag_rows(S, world, r)) for r in range(world)]
+    loc = [qkv[i].cuda() for i in idx]
+    dloc = [dout[i].cuda() for i in idx]
+    for rg in rings:
+        rg.prepare(rows)
+    torch.cuda.synchronize()
+    res_f, res_b = {}, {}
+
+    def fwd(r, ex):
+        res_f[r] = rings[r].forward(loc[r][:, 0].contiguous(), loc[r][:, 1].contiguous(),
+                                    loc[r][:, 2].contiguous())
+
+    vc.run(fwd)
+    torch.cuda.synchronize()
+
+    def bwd(r, ex):
+        o, lse = res_f[r]
+        res_b[r] = rings[r].backward(loc[r][:, 0].contiguous(), loc[r][:, 1].contiguous(),
+                                     loc[r][:, 2].contiguous(), o, lse, dloc[r])
+
+    vc.run(bwd)
+    torch.cuda.synchronize()
+    o = torch.empty(S, H, D)
+    lse = torch.empty(H, S)
+    grads = torch.empty(S, 3, H, D)
+    for r in range(world):
+        o[idx[r]] = res_f[r][0].float().cpu()
+        lse[:, idx[r]] = res_f[r][1].cpu()
+        for i in range(3):
+            grads[idx[r], i] = res_b[r][i].float().cpu()
+    cu = np.array([0, S], np.int32)
+    o_ref, lse_ref = attention_fwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], cu)
+    refs = attention_bwd_ref(qkv[:, 0], qkv[:, 1], qkv[:, 2], dout, cu)
+    e_o = (o - o_ref).abs()
+    e_l = ((lse - lse_ref).abs() / lse_ref.abs().clamp(min=1.0)).max()
+    ok = bool(e_o.max() <= 2e-2 and e_o.mean() <= 2e-3 and e_l <= 1e-3)
+    errs = []
+    for i, rf in enumerate(refs):
+        errs.append(float((grads[:, i] - rf).abs().max()))
+        cos = torch.nn.functional.cosine_similarity(grads[:, i].reshape(1, -1), rf.reshape(1, -1)).item()
+        ok = ok and bool(torch.allclose(grads[:, i], rf, atol=5e-2, rtol=5e-2)) and cos >= 0.999
+    return {"mode": "ring", "tokens": S, "world": world, "heads": H, "o_max": float(e_o.max()),
+            "lse_rel": float(e_l), "grad_max": errs, "ok": ok}
+
+
 def main():
     mode, plan, world, H, D = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), \
         int(sys.argv[5])
     res = {"dense": dense, "sampled": sampled, "stress": stress,
-                                      "shards": shards}[mode](plan, world, H, D)
+                                      "shards": shards, "ring": ring}[mode](plan, world, H, D)
     print(json.dumps(res), flush=True)
     sys.exit(0 if res["ok"] else 1)
 
