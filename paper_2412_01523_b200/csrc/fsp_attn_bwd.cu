@@ -447,6 +447,9 @@ static_assert(kV2Compute == 4 || kV2Compute == 8 || kV2Compute == 16,
 #define FSP_BWD_REDUCE_SPLIT 0  // with 8 reduction warps: 0 = split a unit's 64 columns,
                                 // 1 = split units by parity (each warp drains whole units)
 #endif
+#ifndef FSP_BWD_STAT_SHFL
+#define FSP_BWD_STAT_SHFL 0  // 1: softmax statistics broadcast by warp shuffles, not LDS
+#endif
 #ifndef FSP_BWD_POLY_EVERY
 #define FSP_BWD_POLY_EVERY 0  // one exponential pair in N on the FMA pipe (ex2_poly2); 0 = none
 #endif
@@ -846,10 +849,24 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       const uint64_t sl2x2 = f2(sl2, sl2);
       const uint64_t* nls2 = reinterpret_cast<const uint64_t*>(ls);  // -lse*log2e pairs
       const uint64_t* dl2 = reinterpret_cast<const uint64_t*>(dl);
+#if FSP_BWD_STAT_SHFL
+      // every lane of the warp needs the same kV2Cols statistics: read them once, spread
+      // over the lanes (one conflict-free wavefront per array), and broadcast by shuffles
+      // instead of kV2Cols / 4 broadcast LDS.128 per array (two wavefronts each) — those
+      // wavefronts share the shared-memory pipe with the tensor core's operand reads
+      static_assert(kV2Cols <= 32, "one statistic per lane");
+      const float ls_lane = lane < (uint32_t)kV2Cols ? ls[lane] : 0.f;
+      const float dl_lane = lane < (uint32_t)kV2Cols ? dl[lane] : 0.f;
+#endif
 #pragma unroll
       for (int i = 0; i < kV2Cols; i += 2) {
         const uint64_t x2 =
-            ffma2(f2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sl2x2, nls2[i / 2]);
+            ffma2(f2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sl2x2,
+#if FSP_BWD_STAT_SHFL
+                  f2(__shfl_sync(0xffffffffu, ls_lane, i), __shfl_sync(0xffffffffu, ls_lane, i + 1)));
+#else
+                  nls2[i / 2]);
+#endif
         float p0, p1;
         if (FSP_BWD_POLY_EVERY > 0 && (i / 2) % FSP_BWD_POLY_EVERY == FSP_BWD_POLY_EVERY - 1) {
           ex2_poly2(x2, p0, p1);  // this pair on the FMA pipe, the rest on MUFU
@@ -868,7 +885,13 @@ __global__ void __launch_bounds__(kV2Threads, 1)
           }
         }
         const uint64_t ds2 = fmul2(
-            f2(p0, p1), fsub2(f2(__uint_as_float(dr[i]), __uint_as_float(dr[i + 1])), dl2[i / 2]));
+            f2(p0, p1), fsub2(f2(__uint_as_float(dr[i]), __uint_as_float(dr[i + 1])),
+#if FSP_BWD_STAT_SHFL
+                              f2(__shfl_sync(0xffffffffu, dl_lane, i),
+                                 __shfl_sync(0xffffffffu, dl_lane, i + 1))));
+#else
+                              dl2[i / 2]));
+#endif
         float d0, d1;
         f2_split(ds2, d0, d1);
         pk[i / 2] = pack_bf16(p0, p1);
@@ -937,50 +960,52 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     tc_fence_after();
     constexpr int kEpi = D / (kV2Compute / 4);  // dK/dV columns per compute thread
     const bool kvalid = kv_pos < seqlen;
-    if (!kPersistent && p.sc.degree) {  // (never combined with the persistent launch: the
-      // staging below borrows the Q/dO ring, which a persistent CTA refills for its next entry)
+    if (p.sc.degree) {
       // Fused head->seq (Eq. 4) of dK / dV (destination matrices 1 / 2).  A row's columns
-      // are spread over 4 warps, and per-thread 16-byte stores would cross NVLink as
-      // scattered small packets, so the tile is staged in shared memory (the Q/dO ring,
-      // idle after acc_done; 16-byte chunks XOR-swizzled by row) and written back two full
-      // 256-byte rows per warp instruction.
-      uint8_t* stage = smem + L::kRing;  // dK rows [0, 32 KB), dV rows [32 KB, 64 KB)
-      for (int c = ch * kEpi; c < ch * kEpi + kEpi; c += 32) {
-        uint32_t a[32], b[32];
-        tmem_ld32(tmem + lane_addr + kColDK + c, a);
-        tmem_ld32(tmem + lane_addr + kColDV + c, b);
-        tmem_ld_wait();
+      // are spread over the compute warps, and per-thread 16-byte stores would cross NVLink
+      // as scattered small packets, so each 128-row tile is staged in shared memory first
+      // (16-byte chunks XOR-swizzled by row) and written back two full 256-byte rows per
+      // warp instruction.  Staging space: the two dS^T stages (32 KB) — only these compute
+      // warps write them, and the entry's last dQ^T MMA that read them completed before
+      // acc_done — so dK and dV go through it one after the other.  (The Q/dO ring used
+      // before is refilled by a persistent CTA's producer for its next entry; the dS^T
+      // region is not, which is what lets the fused exchange run on the persistent launch.)
+      uint8_t* stage = smem + L::kDS;
+      for (int mat = 0; mat < 2; ++mat) {
+        const uint32_t col = mat ? kColDV : kColDK;
+        const float mul = mat ? 1.f : p.scale;
+        for (int c = ch * kEpi; c < ch * kEpi + kEpi; c += 32) {
+          uint32_t a[32];
+          tmem_ld32(tmem + lane_addr + col + c, a);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 vk, vv;
-          vk.x = pack_bf16(__uint_as_float(a[i]) * p.scale, __uint_as_float(a[i + 1]) * p.scale);
-          vk.y = pack_bf16(__uint_as_float(a[i + 2]) * p.scale, __uint_as_float(a[i + 3]) * p.scale);
-          vk.z = pack_bf16(__uint_as_float(a[i + 4]) * p.scale, __uint_as_float(a[i + 5]) * p.scale);
-          vk.w = pack_bf16(__uint_as_float(a[i + 6]) * p.scale, __uint_as_float(a[i + 7]) * p.scale);
-          vv.x = pack_bf16(__uint_as_float(b[i]), __uint_as_float(b[i + 1]));
-          vv.y = pack_bf16(__uint_as_float(b[i + 2]), __uint_as_float(b[i + 3]));
-          vv.z = pack_bf16(__uint_as_float(b[i + 4]), __uint_as_float(b[i + 5]));
-          vv.w = pack_bf16(__uint_as_float(b[i + 6]), __uint_as_float(b[i + 7]));
-          const int chunk = ((c + i) >> 3) ^ (r & 15);
-          *reinterpret_cast<uint4*>(stage + r * 256 + chunk * 16) = vk;
-          *reinterpret_cast<uint4*>(stage + 32768 + r * 256 + chunk * 16) = vv;
+          for (int i = 0; i < 32; i += 8) {
+            uint4 vv;
+            vv.x = pack_bf16(__uint_as_float(a[i]) * mul, __uint_as_float(a[i + 1]) * mul);
+            vv.y = pack_bf16(__uint_as_float(a[i + 2]) * mul, __uint_as_float(a[i + 3]) * mul);
+            vv.z = pack_bf16(__uint_as_float(a[i + 4]) * mul, __uint_as_float(a[i + 5]) * mul);
+            vv.w = pack_bf16(__uint_as_float(a[i + 6]) * mul, __uint_as_float(a[i + 7]) * mul);
+            const int chunk = ((c + i) >> 3) ^ (r & 15);
+            *reinterpret_cast<uint4*>(stage + r * 256 + chunk * 16) = vv;
+          }
         }
-      }
-      named_bar_sync(1, 32 * kV2Compute);  // every compute warp's columns are staged
-      const int chunk = lane & 15;
-      for (int pr = cw; pr < 128; pr += kV2Compute) {  // 64 row pairs of dK, then of dV
-        const int mat = pr >> 6;
-        const int srow = 2 * (pr & 63) + (lane >> 4);
-        if (kv0 + srow >= seqlen) continue;
-        const uint4 v = *reinterpret_cast<const uint4*>(stage + mat * 32768 + srow * 256 +
-                                                        ((chunk ^ (srow & 15)) * 16));
-        const int64_t t = seq_start + kv0 + srow;
-        __nv_bfloat16* local = mat ? p.dv : p.dk;
-        if (local)
-          *reinterpret_cast<uint4*>(local + t * (mat ? p.dv_stride : p.dk_stride) +
-                                    (int64_t)head * D + chunk * 8) = v;
-        __nv_bfloat16* prow = scatter_row(p.sc, t, 1 + mat, head, D);
-        if (prow) *reinterpret_cast<uint4*>(prow + chunk * 8) = v;
+        named_bar_sync(1, 32 * kV2Compute);  // every compute warp's columns are staged
+        const int chunk = lane & 15;
+        for (int pr = cw; pr < 64; pr += kV2Compute) {  // 64 row pairs of this matrix
+          const int srow = 2 * pr + (lane >> 4);
+          if (kv0 + srow >= seqlen) continue;
+          const uint4 v = *reinterpret_cast<const uint4*>(stage + srow * 256 +
+                                                          ((chunk ^ (srow & 15)) * 16));
+          const int64_t t = seq_start + kv0 + srow;
+          __nv_bfloat16* local = mat ? p.dv : p.dk;
+          if (local)
+            *reinterpret_cast<uint4*>(local + t * (mat ? p.dv_stride : p.dk_stride) +
+                                      (int64_t)head * D + chunk * 8) = v;
+          __nv_bfloat16* prow = scatter_row(p.sc, t, 1 + mat, head, D);
+          if (prow) *reinterpret_cast<uint4*>(prow + chunk * 8) = v;
+        }
+        // the staging area is reused by the next matrix / the next entry's dS^T
+        named_bar_sync(1, 32 * kV2Compute);
       }
     } else {
       const int64_t trow = (int64_t)(seq_start + kv_pos);
@@ -1142,10 +1167,11 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     p.noncausal = (a->flags & FSP_ATTN_NONCAUSAL) ? 1 : 0;
     if (D == 128) {
       const int smem = BwdSmemV2::kBytes + 1024;
-      // Persistent launch (CTAs steal not-yet-launched entries) unless the head->seq exchange
-      // is fused: its epilogue stages dK/dV in the Q/dO ring the next entry refills.
+      // Persistent launch (CTAs steal not-yet-launched entries), with or without the fused
+      // head->seq exchange (its epilogue stages dK/dV in the dS^T region, which the next
+      // entry does not touch before that epilogue ends); FSP_BWD_PERSISTENT=0: classic.
       const char* env = getenv("FSP_BWD_PERSISTENT");
-      const bool persistent = sc.degree == 0 && !(env && env[0] == '0');
+      const bool persistent = !(env && env[0] == '0');
       if (persistent) {
         FSP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel_v2<true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

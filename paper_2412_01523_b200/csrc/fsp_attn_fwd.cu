@@ -461,6 +461,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   const EntryRing ring{reinterpret_cast<int*>(bars + 24), bars + 20, bars + 22, bars + 26,
                        bars + 25};
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+  // [2] per tile: its 4 softmax warps have read back the O rows they staged in that tile's
+  // Q buffer (fused head->seq epilogue), so the producer may load the next entry's Q there
+  uint64_t* epi_free = bars + 29;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -469,6 +472,8 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_empty, 1);
+    mbar_init(epi_free + 0, 4);
+    mbar_init(epi_free + 1, 4);
     for (int i = 0; i < 2; ++i) {
       mbar_init(ring.full + i, 1);
       mbar_init(ring.empty + i, kRingConsumers);
@@ -508,10 +513,16 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
         uint32_t g0 = 0;  // K/V ring position: kv steps issued by this CTA so far
+        uint32_t n_b = 0;        // entries with a tile B so far
+        bool prev_b = false;     // the previous entry had a tile B
         for (int k = 0;; ++k) {
           const int w = claim_entry<kPersistent>(ring, k);
           if (w >= p.n_tiles) break;
           const PairTile T = decode_pair(p, w);
+          const bool wait_b = prev_b;
+          const uint32_t b_phase = (n_b - 1) & 1;
+          prev_b = T.has_b;
+          n_b += T.has_b ? 1u : 0u;
           if (k > 0) {
             // Q rows of an entry are read by this CTA only: warm L2 while the previous entry
             // finishes, and K_0 / V_0 with them
@@ -522,6 +533,11 @@ __global__ void __launch_bounds__(kF2Threads, 1)
               tma_prefetch_l2_3d(&tm_v, b * 64, T.head, T.seq_start);
             }
             mbar_wait(q_empty, (k - 1) & 1);  // previous entry's QK^T MMAs are done
+            if (p.sc.degree) {
+              // fused head->seq: the previous entry's epilogue stages O in the Q buffers
+              mbar_wait(epi_free + 0, (k - 1) & 1);
+              if (wait_b) mbar_wait(epi_free + 1, b_phase);
+            }
           }
           mbar_expect_tx(bar_q, (T.has_b ? 2 : 1) * L::kTileBytes);
           for (int b = 0; b < 2; ++b) {
@@ -879,9 +895,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       tc_fence_after();
       const float inv_l = 1.f / l;
       const bool valid = q_pos < seqlen;
-      // (the staged path borrows this entry's Q buffer, which a persistent CTA refills for
-      // its next entry: the host never combines the fused exchange with the persistent launch)
-      if (!kPersistent && p.sc.degree) {
+      // (the staged path borrows this entry's Q buffer; a persistent CTA's producer waits on
+      // epi_free before refilling it for the next entry)
+      if (p.sc.degree) {
         // Fused head->seq (Eq. 4): O goes to its owner's sequence shard over NVLink as well
         // as to the local buffer.  One-row-per-thread 16-byte stores would cross NVLink as
         // 32 scattered 16-byte packets per warp instruction, so the warp first stages its
@@ -918,6 +934,8 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           __nv_bfloat16* prow = scatter_row(p.sc, t, 0, head, D);
           if (prow) *reinterpret_cast<uint4*>(prow + chunk * 8) = v;
         }
+        __syncwarp();  // every lane's staged reads are done
+        if (lane == 0) mbar_arrive(epi_free + x);
       } else {
         __nv_bfloat16* orow =
             p.o + (int64_t)(seq_start + q_pos) * p.o_stride + (int64_t)head * D;
@@ -988,7 +1006,7 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
     // QK^T overlap the previous entry's softmax tail and epilogue) unless the head->seq
     // exchange is fused, whose epilogue stages rows in the entry's Q buffer.
     const char* env = getenv("FSP_FWD_PERSISTENT");
-    const bool persistent = p.sc.degree == 0 && !(env && env[0] == '0');
+    const bool persistent = !(env && env[0] == '0');
     if (persistent) {
       FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel<true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
