@@ -849,6 +849,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       const uint64_t sl2x2 = f2(sl2, sl2);
       const uint64_t* nls2 = reinterpret_cast<const uint64_t*>(ls);  // -lse*log2e pairs
       const uint64_t* dl2 = reinterpret_cast<const uint64_t*>(dl);
+      if (FSP_BWD_ABLATE & 128) {  // profiling ablation: statistics from registers, no LDS
+        nls2 = reinterpret_cast<const uint64_t*>(&p.scale);  // (any address: unused below)
+      }
 #if FSP_BWD_STAT_SHFL
       // every lane of the warp needs the same kV2Cols statistics: read them once, spread
       // over the lanes (one conflict-free wavefront per array), and broadcast by shuffles
@@ -865,10 +868,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
 #if FSP_BWD_STAT_SHFL
                   f2(__shfl_sync(0xffffffffu, ls_lane, i), __shfl_sync(0xffffffffu, ls_lane, i + 1)));
 #else
-                  nls2[i / 2]);
+                  (FSP_BWD_ABLATE & 128) ? f2(-8.f, -8.f) : nls2[i / 2]);
 #endif
         float p0, p1;
-        if (FSP_BWD_POLY_EVERY > 0 && (i / 2) % FSP_BWD_POLY_EVERY == FSP_BWD_POLY_EVERY - 1) {
+        constexpr int kPolyEvery = FSP_BWD_POLY_EVERY > 0 ? FSP_BWD_POLY_EVERY : 1;
+        if (FSP_BWD_POLY_EVERY > 0 && (i / 2) % kPolyEvery == kPolyEvery - 1) {
           ex2_poly2(x2, p0, p1);  // this pair on the FMA pipe, the rest on MUFU
         } else {
           float x0, x1;
@@ -890,7 +894,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                               f2(__shfl_sync(0xffffffffu, dl_lane, i),
                                  __shfl_sync(0xffffffffu, dl_lane, i + 1))));
 #else
-                              dl2[i / 2]));
+                              (FSP_BWD_ABLATE & 128) ? f2(0.25f, 0.25f) : dl2[i / 2]));
 #endif
         float d0, d1;
         f2_split(ds2, d0, d1);
@@ -915,7 +919,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       // dS^T row r, query columns [ch*kV2Cols, +kV2Cols) of this half: 16-byte chunks
       uint8_t* row = smem + L::kDS + h * 16384 + r * 128;
 #pragma unroll
-      for (int v = 0; v < kV2Cols / 8; ++v) {
+      for (int v = 0; v < ((FSP_BWD_ABLATE & 256) ? 0 : kV2Cols / 8); ++v) {  // 256: no dS^T STS
         const int chunk = ((int)ch * (kV2Cols / 8) + v) ^ (r & 7);
         *reinterpret_cast<uint4*>(row + chunk * 16) =
             make_uint4(dk[4 * v], dk[4 * v + 1], dk[4 * v + 2], dk[4 * v + 3]);

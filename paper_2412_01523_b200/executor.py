@@ -120,7 +120,8 @@ class FlexSPExecutor:
 
     def __init__(self, world_size: int, rank: int, n_heads: int, head_dim: int,
                  device: torch.device | str = "cuda", softmax_scale: float | None = None,
-                 group=None, fuse_head2seq: bool = True, heap_factory=None):
+                 group=None, fuse_head2seq: bool = True, heap_factory=None,
+                 output_slots: int = 1):
         if head_dim not in (64, 128):
             raise ValueError("head_dim must be 64 or 128")
         self.world_size = world_size
@@ -146,6 +147,12 @@ class FlexSPExecutor:
         # symmetric-memory heap.  vranks.VirtualCluster passes per-virtual-rank heaps that
         # live on one device (the single-GPU multi-rank harness).
         self.heap_factory = heap_factory
+        # 2: out_local / dqkv_local alternate between two heap slots by micro-batch, so
+        # step_from_host can copy a micro-batch's results to the host while the next one
+        # computes; 1 (default): one slot, half the output memory
+        if output_slots not in (1, 2):
+            raise ValueError("output_slots must be 1 or 2")
+        self.output_slots = output_slots
 
     # ------------------------------------------------------------ planning -> tables
     def prepare(self, plan: Any, lengths: Sequence[int], sharded_loader: bool = False) -> StepPlan:
@@ -212,10 +219,11 @@ class FlexSPExecutor:
         # out_local / dqkv_local alternate between two slots (micro-batch parity), so a
         # micro-batch's results can be read out (step_from_host's D2H copy) while the next
         # micro-batch computes into the other slot
+        two = self.output_slots == 2
         for name, elems in (("qkv_recv", 3 * max_recv), ("out_local0", max_local * hd),
-                            ("out_local1", max_local * hd), ("do_recv", max_recv),
+                            ("out_local1", max_local * hd if two else 0), ("do_recv", max_recv),
                             ("dqkv_local0", 3 * max_local * hd),
-                            ("dqkv_local1", 3 * max_local * hd),
+                            ("dqkv_local1", 3 * max_local * hd if two else 0),
                             # step_from_shards: scattered loader rows (q/k/v, dO)
                             ("in_qkv", 3 * max_local * hd if sharded_loader else 0),
                             ("in_do", max_local * hd if sharded_loader else 0)):
@@ -257,11 +265,11 @@ class FlexSPExecutor:
         return self.epoch
 
     # ------------------------------------------------------------ one micro-batch
-    def _out_off(self, sp: StepPlan) -> int:
-        return sp.offsets[f"out_local{self._n_fwd & 1}"]   # slot of the current forward
+    def _out_off(self, sp: StepPlan) -> int:  # slot of the current forward
+        return sp.offsets[f"out_local{self._n_fwd % self.output_slots}"]
 
-    def _dqkv_off(self, sp: StepPlan) -> int:
-        return sp.offsets[f"dqkv_local{self._n_bwd & 1}"]  # slot of the current backward
+    def _dqkv_off(self, sp: StepPlan) -> int:  # slot of the current backward
+        return sp.offsets[f"dqkv_local{self._n_bwd % self.output_slots}"]
 
     def local_buffers(self, sp: StepPlan, mb: RankMicroBatch):
         """Views of this rank's output buffers (inside the heap) for the micro-batch whose
@@ -474,6 +482,8 @@ class FlexSPExecutor:
         copy-out finished).  The copies are in flight when this returns:
         `d2h_stream` orders after them.
         """
+        if host_out is not None and self.output_slots != 2:
+            raise ValueError("copying results to the host needs FlexSPExecutor(output_slots=2)")
         cur = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_h2d_stream"):
             self._h2d_stream = torch.cuda.Stream(self.device)
@@ -535,15 +545,15 @@ class FlexSPExecutor:
             q = bufs[k][0][:rows * 3 * hd].view(rows, 3, self.n_heads, self.head_dim)
             d = bufs[k][1][:rows * hd].view(rows, self.n_heads, self.head_dim)
             # the output slots this micro-batch writes must have been copied out already
-            cur.wait_event(self._out_read[(self._n_fwd + 1) & 1])
+            cur.wait_event(self._out_read[(self._n_fwd + 1) % self.output_slots])
             out, saved = self.micro_batch_forward(sp, mb, q)
-            cur.wait_event(self._dqkv_read[(self._n_bwd + 1) & 1])
+            cur.wait_event(self._dqkv_read[(self._n_bwd + 1) % self.output_slots])
             dqkv = self.micro_batch_backward(sp, mb, saved, d)
             if sink is not None:
                 sink(m, out, dqkv)
             consumed[k].record(cur)
             if host_out is not None and out is not None and rows:
-                so, sd = self._n_fwd & 1, self._n_bwd & 1
+                so, sd = self._n_fwd % self.output_slots, self._n_bwd % self.output_slots
                 self.d2h_stream.wait_stream(cur)
                 with torch.cuda.stream(self.d2h_stream):
                     host_out[m].view(rows, hd).copy_(out.reshape(rows, hd), non_blocking=True)

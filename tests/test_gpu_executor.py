@@ -229,7 +229,7 @@ def test_step_from_host_matches_device_step():
     H, D = 4, 128
     lengths = [700, 1, 130, 2048, 64, 300]
     plan = _plan_n1(lengths, [[3, 1, 5], [0, 2, 4]])
-    ex = FlexSPExecutor(1, 0, H, D, "cuda")
+    ex = FlexSPExecutor(1, 0, H, D, "cuda", output_slots=2)
     sp = ex.prepare(plan, lengths)
     T = sum(lengths)
     g = torch.Generator().manual_seed(3)
