@@ -425,8 +425,43 @@ class FlexSPExecutor:
             if sink is not None:
                 sink(m, out, dqkv)
 
+    # ------------------------------------------------------------ host copy-in / copy-out
+    def _streams(self) -> None:
+        if not hasattr(self, "_h2d_stream"):
+            self._h2d_stream = torch.cuda.Stream(self.device)
+            self.d2h_stream = torch.cuda.Stream(self.device)
+            # persistent across calls: a copy must not overwrite a slot the previous step
+            # is still reading (waiting on a never-recorded event is a no-op)
+            self._h2d_consumed = [torch.cuda.Event() for _ in range(2)]
+            self._h2d_loaded = [torch.cuda.Event() for _ in range(2)]
+            self._out_read = [torch.cuda.Event() for _ in range(2)]   # out_local slot copied out
+            self._dqkv_read = [torch.cuda.Event() for _ in range(2)]  # dqkv_local slot copied out
+            self._h2d_slot = 0            # slot the next copy goes to (strictly alternating)
+            self._h2d_prefetched = None   # (host qkv, host dout, slot) of an in-flight copy
+
+    def _wait_out_slot(self, cur, kind: str) -> None:
+        """Before a forward ("out") / backward ("dqkv"): the output slot it is about to
+        write must have been copied out to the host already."""
+        if kind == "out":
+            cur.wait_event(self._out_read[(self._n_fwd + 1) % self.output_slots])
+        else:
+            cur.wait_event(self._dqkv_read[(self._n_bwd + 1) % self.output_slots])
+
+    def _copy_out(self, cur, m: int, out, dqkv, rows: int, host_out, host_dqkv) -> None:
+        """Micro-batch m's O / dQKV to pinned host memory on the D2H stream."""
+        if host_out is None or out is None or not rows:
+            return
+        hd = self.n_heads * self.head_dim
+        so, sd = self._n_fwd % self.output_slots, self._n_bwd % self.output_slots
+        self.d2h_stream.wait_stream(cur)
+        with torch.cuda.stream(self.d2h_stream):
+            host_out[m].view(rows, hd).copy_(out.reshape(rows, hd), non_blocking=True)
+            host_dqkv[m].view(rows, 3 * hd).copy_(dqkv.reshape(rows, 3 * hd), non_blocking=True)
+            self._out_read[so].record(self.d2h_stream)
+            self._dqkv_read[sd].record(self.d2h_stream)
+
     def step_from_shards(self, sp: StepPlan, shard_qkv: torch.Tensor, shard_dout: torch.Tensor,
-                         sink=None) -> None:
+                         sink=None, host_out=None, host_dqkv=None) -> None:
         """The step fed by the data loader's shards (prepare(..., sharded_loader=True)).
 
         shard_qkv [n_shard, 3, H, D] / shard_dout [n_shard, H, D] hold this rank's loader
@@ -435,12 +470,18 @@ class FlexSPExecutor:
         (fsp_scatter_rows, NVSwitch peer stores into their heap input buffers, PAPER.md:922
         "scatters the data into the corresponding group"); a world barrier before the
         scatter frees the input buffers, one after it publishes the data; the micro-batch
-        then runs on the received loader-order rows exactly as in step()."""
+        then runs on the received loader-order rows exactly as in step().  With host_out /
+        host_dqkv (pinned, per micro-batch) the results go back to the host as in
+        step_from_host (needs output_slots=2)."""
         if sp.shard_tokens is None:
             raise ValueError("prepare the plan with sharded_loader=True first")
+        if host_out is not None and self.output_slots != 2:
+            raise ValueError("copying results to the host needs FlexSPExecutor(output_slots=2)")
         n_shard = int(sp.shard_tokens.shape[0])
         if shard_qkv.shape[0] != n_shard or shard_dout.shape[0] != n_shard:
             raise ValueError(f"rank {self.rank} shard has {n_shard} rows")
+        self._streams()
+        cur = torch.cuda.current_stream(self.device)
         hd = self.n_heads * self.head_dim
         world = range(0, self.world_size)
         off = sp.offsets
@@ -458,10 +499,52 @@ class FlexSPExecutor:
                                torch.bfloat16)
             d = self.heap.view(off["in_do"], (mb.n_local, self.n_heads, self.head_dim),
                                torch.bfloat16)
+            self._wait_out_slot(cur, "out")
             out, saved = self.micro_batch_forward(sp, mb, q)
+            self._wait_out_slot(cur, "dqkv")
             dqkv = self.micro_batch_backward(sp, mb, saved, d)
             if sink is not None:
                 sink(m, out, dqkv)
+            self._copy_out(cur, m, out, dqkv, mb.n_local, host_out, host_dqkv)
+
+    def step_from_host_shards(self, sp: StepPlan, host_shard_qkv: torch.Tensor,
+                              host_shard_dout: torch.Tensor, host_out=None, host_dqkv=None,
+                              sink=None, prefetch_next: tuple | None = None) -> None:
+        """The data-loader path end to end at N > 1: this rank's loader shard arrives from
+        pinned host memory (H2D on the side stream into a double buffer; `prefetch_next =
+        (next_host_shard_qkv, next_host_shard_dout)` uploads the next step's shard while
+        this step computes), is scattered to the plan's groups over NVSwitch
+        (step_from_shards) and the results go back to pinned host memory."""
+        self._streams()
+        cur = torch.cuda.current_stream(self.device)
+        side = self._h2d_stream
+        n = int(host_shard_qkv.shape[0])
+        hd = self.n_heads * self.head_dim
+
+        def upload(hq, hdo):
+            k = self._h2d_slot
+            self._h2d_slot ^= 1
+            q = self._workspace(f"shard_qkv{k}", max(n, 1) * 3 * hd, torch.bfloat16)
+            d = self._workspace(f"shard_do{k}", max(n, 1) * hd, torch.bfloat16)
+            with torch.cuda.stream(side):
+                side.wait_event(self._h2d_consumed[k])
+                if n:
+                    q[:n * 3 * hd].view(n, 3 * hd).copy_(hq.view(n, 3 * hd), non_blocking=True)
+                    d[:n * hd].view(n, hd).copy_(hdo.view(n, hd), non_blocking=True)
+                self._h2d_loaded[k].record(side)
+            return k
+
+        pf, self._h2d_prefetched = self._h2d_prefetched, None
+        k = pf[2] if (pf is not None and pf[0] is host_shard_qkv and pf[1] is host_shard_dout) \
+            else upload(host_shard_qkv, host_shard_dout)
+        if prefetch_next is not None:
+            nk = upload(*prefetch_next)
+            self._h2d_prefetched = (prefetch_next[0], prefetch_next[1], nk)
+        cur.wait_event(self._h2d_loaded[k])
+        q = self._ws[f"shard_qkv{k}"][:n * 3 * hd].view(n, 3, self.n_heads, self.head_dim)
+        d = self._ws[f"shard_do{k}"][:n * hd].view(n, self.n_heads, self.head_dim)
+        self.step_from_shards(sp, q, d, sink=sink, host_out=host_out, host_dqkv=host_dqkv)
+        self._h2d_consumed[k].record(cur)
 
     def step_from_host(self, sp: StepPlan, host_qkv: Sequence[torch.Tensor],
                        host_dout: Sequence[torch.Tensor], host_out: Sequence[torch.Tensor] | None = None,
@@ -485,17 +568,7 @@ class FlexSPExecutor:
         if host_out is not None and self.output_slots != 2:
             raise ValueError("copying results to the host needs FlexSPExecutor(output_slots=2)")
         cur = torch.cuda.current_stream(self.device)
-        if not hasattr(self, "_h2d_stream"):
-            self._h2d_stream = torch.cuda.Stream(self.device)
-            self.d2h_stream = torch.cuda.Stream(self.device)
-            # persistent across calls: a copy must not overwrite a slot the previous step
-            # is still reading (waiting on a never-recorded event is a no-op)
-            self._h2d_consumed = [torch.cuda.Event() for _ in range(2)]
-            self._h2d_loaded = [torch.cuda.Event() for _ in range(2)]
-            self._out_read = [torch.cuda.Event() for _ in range(2)]   # out_local slot copied out
-            self._dqkv_read = [torch.cuda.Event() for _ in range(2)]  # dqkv_local slot copied out
-            self._h2d_slot = 0            # slot the next copy goes to (strictly alternating)
-            self._h2d_prefetched = None   # (host qkv, host dout, slot) of an in-flight copy
+        self._streams()
         side = self._h2d_stream
         consumed, loaded = self._h2d_consumed, self._h2d_loaded
         n = len(sp.micro_batches)
@@ -545,19 +618,11 @@ class FlexSPExecutor:
             q = bufs[k][0][:rows * 3 * hd].view(rows, 3, self.n_heads, self.head_dim)
             d = bufs[k][1][:rows * hd].view(rows, self.n_heads, self.head_dim)
             # the output slots this micro-batch writes must have been copied out already
-            cur.wait_event(self._out_read[(self._n_fwd + 1) % self.output_slots])
+            self._wait_out_slot(cur, "out")
             out, saved = self.micro_batch_forward(sp, mb, q)
-            cur.wait_event(self._dqkv_read[(self._n_bwd + 1) % self.output_slots])
+            self._wait_out_slot(cur, "dqkv")
             dqkv = self.micro_batch_backward(sp, mb, saved, d)
             if sink is not None:
                 sink(m, out, dqkv)
             consumed[k].record(cur)
-            if host_out is not None and out is not None and rows:
-                so, sd = self._n_fwd % self.output_slots, self._n_bwd % self.output_slots
-                self.d2h_stream.wait_stream(cur)
-                with torch.cuda.stream(self.d2h_stream):
-                    host_out[m].view(rows, hd).copy_(out.reshape(rows, hd), non_blocking=True)
-                    host_dqkv[m].view(rows, 3 * hd).copy_(dqkv.reshape(rows, 3 * hd),
-                                                         non_blocking=True)
-                    self._out_read[so].record(self.d2h_stream)
-                    self._dqkv_read[sd].record(self.d2h_stream)
+            self._copy_out(cur, m, out, dqkv, rows, host_out, host_dqkv)

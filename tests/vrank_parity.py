@@ -272,7 +272,7 @@ def shards(plan_name, world, H, D):
     res = dense(plan_name, world, H, D)  # plain step vs oracle (and its outputs below)
     plan = load_plan(plan_name)
     lengths = plan["lengths"]
-    vc = VirtualCluster(world, H, D, "cuda")
+    vc = VirtualCluster(world, H, D, "cuda", output_slots=2)
     sps = vc.prepare(plan, lengths, sharded_loader=True)
     T = sum(lengths)
     g = torch.Generator().manual_seed(2024)
@@ -331,8 +331,34 @@ def shards(plan_name, world, H, D):
     ok = routes_ok and scatter_exact and bool(torch.isfinite(o).all()) and e_o.max() <= 2e-2
     for i, r in enumerate(refs):
         ok = ok and bool(torch.allclose(dq[:, i], r, atol=5e-2, rtol=5e-2))
+    # the host-fed form (pinned shard in, O / dQKV back to pinned memory), twice with the
+    # next step's shard prefetched: the host results equal the device step's bit for bit
+    # (dQ to its atomics' order)
+    hsq = [t.cpu().pin_memory() for t in sq]
+    hsd = [t.cpu().pin_memory() for t in sd]
+    ho = [[torch.zeros((mb.n_local, H, D), dtype=torch.bfloat16).pin_memory()
+           for mb in sp.micro_batches] for sp in sps]
+    hg = [[torch.zeros((mb.n_local, 3, H, D), dtype=torch.bfloat16).pin_memory()
+           for mb in sp.micro_batches] for sp in sps]
+    for it in range(2):
+        vc.run(lambda r, ex: ex.step_from_host_shards(
+            sps[r], hsq[r], hsd[r], host_out=ho[r], host_dqkv=hg[r],
+            prefetch_next=(hsq[r], hsd[r]) if it == 0 else None))
+        for s_ in vc.streams:
+            s_.wait_stream(vc.executors[0].d2h_stream)
+        for ex in vc.executors:
+            torch.cuda.current_stream().wait_stream(ex.d2h_stream)
+        torch.cuda.synchronize()
+    host_ok = True
+    for (r, m), (out, dqkv) in got.items():
+        host_ok = host_ok and torch.equal(ho[r][m], out.cpu()) and \
+            torch.equal(hg[r][m][:, 1:], dqkv[:, 1:].cpu()) and \
+            bool(torch.allclose(hg[r][m][:, 0].float(), dqkv[:, 0].float().cpu(), atol=1e-2,
+                                rtol=1e-2))
+    ok = ok and host_ok
     res.update({"mode": "shards", "routes_match_oracle": routes_ok,
-                "scatter_bit_exact": scatter_exact, "shard_o_max": float(e_o.max())})
+                "scatter_bit_exact": scatter_exact, "host_fed_equal": host_ok,
+                "shard_o_max": float(e_o.max())})
     res["ok"] = bool(res["ok"] and ok)
     return res
 
