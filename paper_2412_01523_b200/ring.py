@@ -74,7 +74,8 @@ def _merge(o, lse, o_p, lse_p):
 class RingAttention:
     """Ring attention over a CP group of `degree` ranks (contiguous rank block starting at
     `rank_begin`), on the peer heap `heap` (executor.PeerHeap or vranks.VirtualHeap; one
-    per rank, identical carving).  forward(q, k, v) -> (o, lse) and
+    per rank, identical carving).  The heap must be its own (not an executor's): the ring
+    carves it from offset 0 and runs its own barrier epochs on its signal page.  forward(q, k, v) -> (o, lse) and
     backward(q, k, v, o, lse, do) -> (dq, dk, dv) on the local zig-zag rows
     ([2c, H, D] bf16 each); every member calls them in the same order."""
 
