@@ -38,7 +38,18 @@ FULLSIZE = [(4, "c2_n4_flexsp.json", 32, 128), (8, "c2_n8_static.json", 32, 128)
             (8, "c4_n8_flexsp.json", 52, 128)]
 
 
+def _release_gpu_memory():
+    """The subprocesses below need most of the GPU: hand back what earlier tests of this
+    pytest process left in torch's caching allocator."""
+    import gc
+    gc.collect()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+
 def _run(cmd, timeout, env_extra=None):
+    _release_gpu_memory()
     env = dict(os.environ, OMP_NUM_THREADS="4", FSP_BARRIER_TIMEOUT_S="120")
     env.update(env_extra or {})
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)

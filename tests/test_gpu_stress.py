@@ -126,6 +126,9 @@ def test_fused_scatter_and_exchange_guard_bands():
 @pytest.mark.parametrize("n,plan,heads", [(8, "rand1_n8_flexsp.json", 13), (8, "tiny_n8.json", 8),
                                           (4, "idle_n4.json", 8)])
 def test_virtual_rank_barrier_stress(n, plan, heads):
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # the subprocess gets the GPU memory earlier tests cached
     env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", CUDA_MODULE_LOADING="EAGER",
                FSP_BARRIER_TIMEOUT_S="120")
     res = subprocess.run([sys.executable, str(ROOT / "tests" / "vrank_parity.py"), "stress", plan,
