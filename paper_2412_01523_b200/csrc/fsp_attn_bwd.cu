@@ -769,7 +769,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       for (int i = 0; i < 8; ++i) atomicAdd(&g_bwd_wait[i], (unsigned long long)tw[i]);
       atomicAdd(&g_bwd_wait[8], (unsigned long long)units);
       __threadfence();
-      if (atomicAdd(&g_bwd_done, 1u) == gridDim.x - 1) {
+      // persistent launches: only the first ~148 CTAs run (the rest are cancelled by CLC)
+      if (atomicAdd(&g_bwd_done, 1u) == (kPersistent ? min(gridDim.x, 148u) : gridDim.x) - 1) {
         printf("bwd MMA issuer cycles (sum over CTAs): units %llu total %llu | ring_full(Q) %llu "
                "tm_free(dP) %llu ring_full(dO) %llu p_ready %llu tm_free(dQ) %llu kv %llu\n",
                g_bwd_wait[8], g_bwd_wait[7], g_bwd_wait[0], g_bwd_wait[1], g_bwd_wait[2],

@@ -663,7 +663,8 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         for (int i = 0; i < 8; ++i) atomicAdd(&g_fwd_wait[i], (unsigned long long)tw[i]);
         atomicAdd(&g_fwd_wait[8], (unsigned long long)steps);
         __threadfence();
-        if (atomicAdd(&g_fwd_done, 1u) == gridDim.x - 1) {
+        // persistent launches: only the first ~148 CTAs run (the rest are cancelled by CLC)
+        if (atomicAdd(&g_fwd_done, 1u) == (kPersistent ? min(gridDim.x, 148u) : gridDim.x) - 1) {
           printf("fwd MMA issuer cycles (sum over CTAs): tile-steps %llu total %llu | p_half A %llu "
                  "p_half B %llu k_full %llu v_full %llu q %llu\n", g_fwd_wait[8], g_fwd_wait[7],
                  g_fwd_wait[0], g_fwd_wait[1], g_fwd_wait[2], g_fwd_wait[3], g_fwd_wait[5]);

@@ -157,3 +157,21 @@ def test_scatter_routes_match_oracle_on_golden_plans():
                 assert [tuple(x) for x in got.tolist()] == ref[r], (name, r)
                 delivered += got.shape[0]
         assert delivered == sum(lengths)
+
+
+def test_ring_zigzag_chunks_cover_the_sequence():
+    """Context parallelism (ring.py): rank r's local rows are chunks r and 2R-1-r; every
+    position of the sequence belongs to exactly one rank, each rank holds the same number of
+    rows, and the causal work (positions below each row) is balanced within 1/R."""
+    from paper_2412_01523_b200.ring import RingLayout, zigzag_rows
+    for R in (1, 2, 4, 8):
+        S = 2 * R * 96
+        rows = [zigzag_rows(S, R, r) for r in range(R)]
+        assert sorted(np.concatenate(rows).tolist()) == list(range(S))
+        assert len({len(x) for x in rows}) == 1
+        work = [int((x + 1).sum()) for x in rows]
+        assert max(work) - min(work) <= S * S // (2 * R) // R
+        off = RingLayout(S // R, 4, 128).offsets(R)
+        assert off["kv"] % 4096 == 0 and off["dkv"] % 4096 == 0 and off["end"] > off["dkv"]
+    with pytest.raises(ValueError):
+        zigzag_rows(1000, 3, 0)
