@@ -334,3 +334,36 @@ def test_flexsp_attention_autograd_two_layers():
         assert torch.equal(grad[:, 1:], d_ref[:, 1:]), key  # dK, dV: one writer per row
         # dQ sums fp32 reductions from several CTAs in whatever order they land
         torch.testing.assert_close(grad[:, 0].float(), d_ref[:, 0].float(), atol=1e-2, rtol=1e-2)
+
+
+def test_step_from_host_shards_single_rank():
+    """The data-loader path at one rank: the whole batch is the shard, the per-plan scatter
+    is a local copy through the route table, results come back to pinned host memory —
+    equal to the device step (O, dK, dV bit for bit; dQ to its atomics' order)."""
+    from paper_2412_01523_b200.executor import FlexSPExecutor
+    H, D = 4, 128
+    lengths = [700, 1, 130, 2048, 64, 300]
+    plan = _plan_n1(lengths, [[3], [1, 5, 0], [2, 4]])
+    ex = FlexSPExecutor(1, 0, H, D, "cuda", output_slots=2)
+    sp = ex.prepare(plan, lengths, sharded_loader=True)
+    T = sum(lengths)
+    assert sp.shard_tokens.tolist() == list(range(T))
+    g = torch.Generator().manual_seed(9)
+    qkv = torch.randn(T, 3, H, D, generator=g).bfloat16()
+    dout = torch.randn(T, H, D, generator=g).bfloat16()
+    toks = [torch.from_numpy(mb.local_tokens) for mb in sp.micro_batches]
+    ref = {}
+    ex.step(sp, [qkv[t].cuda() for t in toks], [dout[t].cuda() for t in toks],
+            sink=lambda m, o, d: ref.__setitem__(m, (o.cpu(), d.cpu())))
+    ho = [torch.zeros((t.numel(), H, D), dtype=torch.bfloat16).pin_memory() for t in toks]
+    hg = [torch.zeros((t.numel(), 3, H, D), dtype=torch.bfloat16).pin_memory() for t in toks]
+    hq, hd = qkv.pin_memory(), dout.pin_memory()
+    for it in range(3):
+        ex.step_from_host_shards(sp, hq, hd, host_out=ho, host_dqkv=hg,
+                                 prefetch_next=(hq, hd) if it < 2 else None)
+    torch.cuda.current_stream().wait_stream(ex.d2h_stream)
+    torch.cuda.synchronize()
+    for m in range(len(toks)):
+        assert torch.equal(ho[m], ref[m][0])
+        assert torch.equal(hg[m][:, 1:], ref[m][1][:, 1:])
+        torch.testing.assert_close(hg[m][:, 0].float(), ref[m][1][:, 0].float(), atol=1e-2, rtol=1e-2)
