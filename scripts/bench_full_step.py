@@ -68,6 +68,9 @@ def main():
         zs = ZeroStack(layers, world, rank, optimizer=args.optimizer)
         torch.cuda.empty_cache()
     ex = FlexSPExecutor(world, rank, HEADS, HIDDEN // HEADS, dev)
+    # the peak below is the training steps' (model construction materialises full layers
+    # before ZeRO-3 shards them)
+    torch.cuda.reset_peak_memory_stats(dev)
     strategies = ["flexsp", "static"] if args.strategy == "both" else [args.strategy]
     out = {}
     for strategy in strategies:
