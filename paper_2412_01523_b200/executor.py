@@ -521,16 +521,27 @@ class FlexSPExecutor:
         n = int(host_shard_qkv.shape[0])
         hd = self.n_heads * self.head_dim
 
+        rows = max(n, int(prefetch_next[0].shape[0]) if prefetch_next is not None else 0, 1)
+        have = self._ws.get("shard_do0")
+        if have is None or have.numel() < rows * hd:
+            # the double buffer grows: no copy may still be landing in the old one
+            self._h2d_prefetched = None
+            cur.wait_stream(side)
+            for kk in range(2):
+                self._workspace(f"shard_qkv{kk}", rows * 3 * hd, torch.bfloat16)
+                self._workspace(f"shard_do{kk}", rows * hd, torch.bfloat16)
+
         def upload(hq, hdo):
             k = self._h2d_slot
             self._h2d_slot ^= 1
-            q = self._workspace(f"shard_qkv{k}", max(n, 1) * 3 * hd, torch.bfloat16)
-            d = self._workspace(f"shard_do{k}", max(n, 1) * hd, torch.bfloat16)
+            m_ = int(hq.shape[0])
+            q = self._ws[f"shard_qkv{k}"]
+            d = self._ws[f"shard_do{k}"]
             with torch.cuda.stream(side):
                 side.wait_event(self._h2d_consumed[k])
-                if n:
-                    q[:n * 3 * hd].view(n, 3 * hd).copy_(hq.view(n, 3 * hd), non_blocking=True)
-                    d[:n * hd].view(n, hd).copy_(hdo.view(n, hd), non_blocking=True)
+                if m_:
+                    q[:m_ * 3 * hd].view(m_, 3 * hd).copy_(hq.view(m_, 3 * hd), non_blocking=True)
+                    d[:m_ * hd].view(m_, hd).copy_(hdo.view(m_, hd), non_blocking=True)
                 self._h2d_loaded[k].record(side)
             return k
 
