@@ -457,7 +457,15 @@ constexpr int kV2Reduce = FSP_BWD_REDUCE_WARPS;  // 4 or 8: 1 or 2 warps per lan
 constexpr bool kRedSplitUnits = FSP_BWD_REDUCE_SPLIT && kV2Reduce == 8;
 constexpr int kV2RedCols = kRedSplitUnits ? 64 : 64 / (kV2Reduce / 4);  // dQ^T columns per warp
 constexpr int kTmFreeCount = kRedSplitUnits ? 4 : kV2Reduce;  // warps draining one unit
-constexpr int kV2Threads = 64 + 32 * (kV2Compute + kV2Reduce);
+#ifndef FSP_BWD_WG5
+#define FSP_BWD_WG5 0  // 1: five warpgroups (TMA+MMA+2 idle | 8 compute | 8 reduction split by
+                       // unit parity) with setmaxnreg moving registers to the compute warps
+#endif
+constexpr bool kWG5 = FSP_BWD_WG5;
+static_assert(!kWG5 || (kV2Compute == 8 && kV2Reduce == 8 && kRedSplitUnits),
+              "FSP_BWD_WG5 needs 8 compute and 8 unit-split reduction warps");
+constexpr int kV2Warp0 = kWG5 ? 4 : 2;  // first compute warp (warpgroup-aligned with WG5)
+constexpr int kV2Threads = kWG5 ? 640 : 64 + 32 * (kV2Compute + kV2Reduce);
 constexpr uint32_t kV2ColS = 256, kV2ColDP = 384;
 
 struct BwdSmemV2 {
@@ -617,6 +625,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp < kV2Warp0) {
+  if (kWG5) setmaxnreg_dec<56>();  // warpgroup 0: TMA, MMA and two idle warps
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -784,9 +794,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
 #endif
     }
     __syncwarp();
-  } else if (warp < 2 + kV2Compute) {
+  }
+  } else if (warp < kV2Warp0 + kV2Compute) {
+    if (kWG5) setmaxnreg_inc<144>();
     // ------------------------------------------------------------ compute warps
-    const uint32_t cw = warp - 2;              // 0..kV2Compute-1
+    const uint32_t cw = warp - kV2Warp0;       // 0..kV2Compute-1
     const uint32_t quad = warp & 3;            // TMEM lane quadrant
     const uint32_t ch = cw >> 2;               // which kV2Cols of the 64 columns
     const int r = quad * 32 + lane;            // kv row of S^T / dP^T
@@ -1042,12 +1054,13 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     IT0 += n_it;
     }  // schedule entries
   } else {
+    if (kWG5) setmaxnreg_dec<80>();
     // ------------------------------------------------------------ dQ reduction warps
     // dQ^T(u) in TMEM: lane = d, columns = the half tile's 64 query rows.  dq_accum is
     // [H, T, D] fp32 so a warp's 32 lanes add 128 contiguous bytes per query row and the
     // row stride (D*4 = 512 B) folds into the instruction's immediate offset.
     const uint32_t quad = warp & 3;
-    const int part = (int)(warp - 2 - kV2Compute) >> 2;  // which kV2RedCols of the 64 columns
+    const int part = (int)(warp - kV2Warp0 - kV2Compute) >> 2;  // columns / unit parity
     const int r = quad * 32 + lane;
     const uint32_t lane_addr = (quad * 32u) << 16;
     uint32_t U0 = 0;  // global unit index of the entry's first unit
@@ -1069,7 +1082,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       mbar_wait(dq_full + h, IT & 1);
 #if FSP_BWD_TIMING
       const long long tr1 = clock64();
-      if (warp == 2 + kV2Compute && lane == 0) atomicAdd(&g_bwd_wait[11], (unsigned long long)(tr1 - tr0));
+      if (warp == kV2Warp0 + kV2Compute && lane == 0) atomicAdd(&g_bwd_wait[11], (unsigned long long)(tr1 - tr0));
 #endif
       tc_fence_after();
       if (FSP_BWD_ABLATE & 2) {  // profiling ablation: no dQ readout / reductions
@@ -1117,7 +1130,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                          : "memory");
       }
 #if FSP_BWD_TIMING
-      if (warp == 2 + kV2Compute && lane == 0) atomicAdd(&g_bwd_wait[12], (unsigned long long)(clock64() - tr1));
+      if (warp == kV2Warp0 + kV2Compute && lane == 0) atomicAdd(&g_bwd_wait[12], (unsigned long long)(clock64() - tr1));
 #endif
     }
     U0 += n_u;
