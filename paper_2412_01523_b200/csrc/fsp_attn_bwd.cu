@@ -796,7 +796,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     __syncwarp();
   }
   } else if (warp < kV2Warp0 + kV2Compute) {
-    if (kWG5) setmaxnreg_inc<144>();
+    // a CTA can only move registers it was launched with: 640 x 96 at launch, 40 x 128 freed
+    // by warpgroup 0 and 16 x 256 by the reduction warpgroups pay for 32 x 256 here
+    if (kWG5) setmaxnreg_inc<128>();
     // ------------------------------------------------------------ compute warps
     const uint32_t cw = warp - kV2Warp0;       // 0..kV2Compute-1
     const uint32_t quad = warp & 3;            // TMEM lane quadrant
