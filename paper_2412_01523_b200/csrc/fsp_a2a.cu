@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "fsp_host.h"
+#include "fsp_ptx.cuh"
 
 namespace fsp {
 namespace {
@@ -104,6 +105,101 @@ __global__ void __launch_bounds__(kThreads) a2a_kernel(const uint8_t* __restrict
   }
   // make the peer stores visible system-wide before the group barrier publishes
   __threadfence_system();
+}
+
+// TMA-staged variant (FSP_A2A_TMA=1): every chunk goes global -> shared -> peer memory
+// through the bulk-copy (TMA) engine instead of register loads / stores.  One elected lane
+// per warp runs a kStages-deep ring of chunk buffers: the load of chunk i+1 is in flight
+// while chunk i's bulk store drains, and a buffer is reloaded only after the store that read
+// it has finished reading (bulk wait_group.read).  Pad rows of a seq2head send are stored
+// from a zeroed buffer (their zeros keep garbage out of the attention's masked PV products).
+constexpr int kTmaWarps = 8;
+constexpr int kTmaStages = 3;  // 8 KB x (1 + 8 warps x 3) = 200 KB of shared memory
+constexpr int kTmaChunkMax = 8192;  // bytes of one (row, matrix, peer) head slice
+
+template <bool kSeq2Head>
+__global__ void __launch_bounds__(32 * kTmaWarps) a2a_tma_kernel(const uint8_t* __restrict__ src,
+                                                                 PeerPtrs dst,
+                                                                 const int32_t* __restrict__ index,
+                                                                 FspA2A a) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* zero_buf = sm;  // kTmaChunkMax zero bytes shared by the CTA
+  uint8_t* ring = sm + kTmaChunkMax + warp * kTmaStages * kTmaChunkMax;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kTmaChunkMax * (1 + kTmaWarps * kTmaStages)) +
+                   warp * kTmaStages;
+  for (uint32_t i = threadIdx.x; i < kTmaChunkMax / 16; i += blockDim.x)
+    reinterpret_cast<int4*>(zero_buf)[i] = make_int4(0, 0, 0, 0);
+  if (lane == 0)
+    for (int st = 0; st < kTmaStages; ++st) mbar_init(bars + st, 1);
+  fence_mbar_init();
+  fence_async_smem();  // the zero buffer is read by the async proxy
+  __syncthreads();
+  if (lane != 0) return;
+  const int d = a.degree;
+  int hmax = 0;
+  for (int jj = 0; jj < d; ++jj) hmax = max(hmax, a.head_begin[jj + 1] - a.head_begin[jj]);
+  const int64_t head_bytes = (int64_t)a.head_dim * 2;
+  const int64_t sharded_mat = hmax * head_bytes;
+  const uint32_t n_chunks = (uint32_t)a.rows_per_rank * (uint32_t)a.n_mats * (uint32_t)d;
+  const int64_t src_stride = a.src_stride * 2, dst_stride = a.dst_stride * 2;
+  const int64_t full_row = (int64_t)a.n_heads * head_bytes;
+  const uint32_t warps = gridDim.x * kTmaWarps;
+  // chunk it -> (source, destination, bytes, zero?)
+  auto decode = [&](uint32_t c, const uint8_t*& sp, uint8_t*& dp, uint32_t& bytes) -> int {
+    const uint32_t j = c % d, rm = c / d, m = rm % a.n_mats, i = rm / a.n_mats;
+    if (kSeq2Head) {
+      const int hb = a.head_begin[j];
+      bytes = (uint32_t)((a.head_begin[j + 1] - hb) * head_bytes);
+      const int32_t srow = index ? index[i] : (int32_t)i;
+      sp = srow < 0 ? nullptr : src + (int64_t)srow * src_stride + m * full_row + hb * head_bytes;
+      dp = dst.p[j] + ((int64_t)a.rank * a.rows_per_rank + i) * dst_stride + (int64_t)m * sharded_mat;
+      return srow < 0 ? 1 : 0;  // 1: zero row
+    }
+    const int hb = a.head_begin[a.rank];
+    bytes = (uint32_t)((a.head_begin[a.rank + 1] - hb) * head_bytes);
+    const int32_t drow = index ? index[(int64_t)j * a.rows_per_rank + i] : (int32_t)i;
+    if (drow < 0) return 2;  // pad row: nothing to send
+    sp = src + ((int64_t)j * a.rows_per_rank + i) * src_stride + (int64_t)m * sharded_mat;
+    dp = dst.p[j] + (int64_t)drow * dst_stride + m * full_row + hb * head_bytes;
+    return 0;
+  };
+  uint32_t it = 0;  // chunks loaded by this warp so far
+  uint8_t* p_dp = nullptr;
+  uint32_t p_bytes = 0;
+  int p_kind = 2;
+  for (uint32_t c = blockIdx.x * kTmaWarps + warp;; c += warps) {
+    const bool more = c < n_chunks;
+    const uint8_t* sp = nullptr;
+    uint8_t* dp = nullptr;
+    uint32_t bytes = 0;
+    int kind = 2;
+    if (more) {
+      kind = decode(c, sp, dp, bytes);
+      if (kind == 0) {
+        const int st = it % kTmaStages;
+        // the store that last read this buffer (chunk it - kTmaStages) must have read it
+        if (it >= kTmaStages) bulk_wait_read<kTmaStages - 1>();
+        mbar_expect_tx(bars + st, bytes);
+        bulk_load(ring + st * kTmaChunkMax, sp, bytes, bars + st);
+      }
+    }
+    // store the previous chunk (its load has had this chunk's issue time to land)
+    if (p_kind == 0) {
+      const uint32_t pit = it - 1, st = pit % kTmaStages;
+      mbar_wait(bars + st, (pit / kTmaStages) & 1);
+      bulk_store(p_dp, ring + st * kTmaChunkMax, p_bytes);
+      bulk_commit();
+    } else if (p_kind == 1) {
+      bulk_store(p_dp, zero_buf, p_bytes);
+      bulk_commit();
+    }
+    if (!more) break;
+    if (kind == 0) ++it;
+    p_dp = dp, p_bytes = bytes, p_kind = kind;
+  }
+  bulk_wait0();            // every bulk store of this warp has completed
+  __threadfence_system();  // ... and is visible before the group barrier publishes
 }
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -210,6 +306,21 @@ int launch_a2a(const FspA2A* a, const void* src, void* const* peer_dst, const in
   const int64_t chunks = (int64_t)n.rows_per_rank * n.n_mats * n.degree;
   FSP_CHECK_ARG(chunks < (1ll << 32), "exchange too large");
   if (chunks == 0) return FSP_OK;
+  static const bool use_tma = [] {
+    const char* e = getenv("FSP_A2A_TMA");
+    return e && e[0] == '1';
+  }();
+  if (use_tma && hmax * (int64_t)n.head_dim * 2 <= kTmaChunkMax) {
+    const int smem = kTmaChunkMax * (1 + kTmaWarps * kTmaStages) + kTmaWarps * kTmaStages * 8;
+    int64_t blocks = (chunks + kTmaWarps - 1) / kTmaWarps;
+    if (blocks > 148) blocks = 148;  // one CTA (8 bulk-copy rings) per SM
+    FSP_CUDA(cudaFuncSetAttribute(a2a_tma_kernel<kSeq2Head>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    a2a_tma_kernel<kSeq2Head><<<(unsigned)blocks, 32 * kTmaWarps, smem, (cudaStream_t)stream>>>(
+        reinterpret_cast<const uint8_t*>(src), pp, index, n);
+    FSP_LAUNCH_CHECK();
+    return FSP_OK;
+  }
   int64_t blocks = (chunks + kThreads / 32 - 1) / (kThreads / 32);
   if (blocks > 148 * 8) blocks = 148 * 8;
   a2a_kernel<kSeq2Head><<<(unsigned)blocks, kThreads, 0, (cudaStream_t)stream>>>(
