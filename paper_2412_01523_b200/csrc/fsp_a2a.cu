@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(kThreads) a2a_kernel(const uint8_t* __restrict
   __threadfence_system();
 }
 
-// TMA-staged variant (FSP_A2A_TMA=1): every chunk goes global -> shared -> peer memory
+// TMA-staged path (default; FSP_A2A_TMA=0: the register kernel above): every chunk goes
+// global -> shared -> peer memory
 // through the bulk-copy (TMA) engine instead of register loads / stores.  One elected lane
 // per warp runs a kStages-deep ring of chunk buffers: the load of chunk i+1 is in flight
 // while chunk i's bulk store drains, and a buffer is reloaded only after the store that read
@@ -306,9 +307,11 @@ int launch_a2a(const FspA2A* a, const void* src, void* const* peer_dst, const in
   const int64_t chunks = (int64_t)n.rows_per_rank * n.n_mats * n.degree;
   FSP_CHECK_ARG(chunks < (1ll << 32), "exchange too large");
   if (chunks == 0) return FSP_OK;
+  // TMA bulk-copy path by default (666 vs 652 GB/s at d=2, 1 GB per rank;
+  // profiles/r02_a2a_tma.md); FSP_A2A_TMA=0 selects the register-copy kernel
   static const bool use_tma = [] {
     const char* e = getenv("FSP_A2A_TMA");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   if (use_tma && hmax * (int64_t)n.head_dim * 2 <= kTmaChunkMax) {
     const int smem = kTmaChunkMax * (1 + kTmaWarps * kTmaStages) + kTmaWarps * kTmaStages * 8;
