@@ -23,7 +23,9 @@ def main():
     for path in sys.argv[1:]:
         for (i, name, dev), m in sorted(rows(path).items()):
             t = m["gpu__time_duration.sum"] * 1e-9
-            kind = "seq2head" if "a2a_kernel<1>" in name else "head2seq"  # template arg = kSeq2Head
+            seq = any(t in name for t in ("a2a_kernel<1>", "a2a_kernel<true>", "a2a_tma_kernel<1>",
+                                          "a2a_tma_kernel<true>"))
+            kind = ("seq2head" if seq else "head2seq") + (" (TMA)" if "tma" in name else "")
             u, tot = m["nvltx__bytes_data_user.sum"], m["nvltx__bytes.sum"]
             print(f"| {path.split('/')[-1]} | {i} | {kind} | {dev} | {t * 1e6:.0f} | {u / 1e6:.1f} | "
                   f"{tot / 1e6:.1f} | {u / t / 1e9:.0f} | {tot / t / 1e9:.0f} | "
