@@ -106,7 +106,8 @@ def main():
                 o1, lse1 = ops_.attn_fwd(*(full[:, i, h].contiguous().view(S, 1, D) for i in range(3)),
                                          sched1)
                 res = check_sequence(qh, kh, vh, dh, o_rows, dq_rows, dk_rows, dv_rows,
-                                     o1[:, 0], lse1[0], qrows, krows, f"ring S={S} head {h}")
+                                     o1[:, 0].cpu(), lse1[0].cpu(), qrows, krows,
+                                     f"ring S={S} head {h}")
                 ring_lse = torch.stack([at[t][1][h] for t in qrows])
                 res["ring_lse_vs_single_gpu_max"] = float((ring_lse - lse1[0, qrows].cpu()).abs().max())
                 res["ok"] = res["ok"] and res["ring_lse_vs_single_gpu_max"] <= 1e-2
