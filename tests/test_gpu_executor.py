@@ -367,3 +367,52 @@ def test_step_from_host_shards_single_rank():
         assert torch.equal(ho[m], ref[m][0])
         assert torch.equal(hg[m][:, 1:], ref[m][1][:, 1:])
         torch.testing.assert_close(hg[m][:, 0].float(), ref[m][1][:, 0].float(), atol=1e-2, rtol=1e-2)
+
+
+@pytest.mark.parametrize("degree,H", [(2, 4), (4, 10)])
+def test_fused_head2seq_persistent_matches_classic(degree, H, monkeypatch):
+    """The fused head->seq epilogues on the persistent launches (the forward producer waits
+    on epi_free before refilling the Q buffer the epilogue staged O in; the backward stages
+    dK / dV through the dS^T region) write exactly what the classic one-CTA-per-entry launch
+    writes — with far more schedule entries than SMs, so CTAs run several entries each."""
+    ops = _ops()
+    from paper_2412_01523_b200.layout import build_microbatch_layout, head_split
+    D = 128
+    lengths = [300] * 240 + [1, 129, 2048, 777]
+    mb = {"selected_groups": [{"slot_id": 0, "degree": degree,
+                               "sequence_indices": list(range(len(lengths)))}]}
+    grp = build_microbatch_layout(mb, lengths, degree, n_heads=H).groups[0]
+    hb = head_split(H, degree)
+    R, T = grp.rows_per_rank, grp.padded_tokens
+    n_loc = [int((grp.shard(j) >= 0).sum()) for j in range(degree)]
+    table = torch.from_numpy(np.ascontiguousarray(grp.unpack_table().reshape(-1))).cuda()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    ins = []
+    for j in range(degree):
+        hn = hb[j + 1] - hb[j]
+        ins.append((torch.randn((T, 3, hn, D), generator=g, device="cuda", dtype=torch.bfloat16),
+                    torch.randn((T, hn, D), generator=g, device="cuda", dtype=torch.bfloat16)))
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("FSP_FWD_PERSISTENT", mode)
+        monkeypatch.setenv("FSP_BWD_PERSISTENT", mode)
+        outs = [torch.zeros(n, H, D, dtype=torch.bfloat16, device="cuda") for n in n_loc]
+        grads = [torch.zeros(n, 3, H, D, dtype=torch.bfloat16, device="cuda") for n in n_loc]
+        for j in range(degree):
+            hn = hb[j + 1] - hb[j]
+            sched = ops.AttnSchedule.build(grp.cu_seqlens, "cuda", hn, total_rows=T, head_dim=D)
+            if mode == "1":
+                assert sched.n_fwd > 148 and sched.n_bwd > 148
+            qkv, dout = ins[j]
+            sc = ops.HeadScatter(degree, R, hb[j], H * D, 0, table, [t.data_ptr() for t in outs])
+            o, lse = ops.attn_fwd(qkv[:, 0], qkv[:, 1], qkv[:, 2], sched, scatter=sc)
+            sc2 = ops.HeadScatter(degree, R, hb[j], 3 * H * D, H * D, table,
+                                  [t.data_ptr() for t in grads])
+            ops.attn_bwd(qkv[:, 0], qkv[:, 1], qkv[:, 2], o, dout, lse, sched, scatter=sc2)
+        torch.cuda.synchronize()
+        res[mode] = (outs, grads)
+    for j in range(degree):
+        assert torch.equal(res["0"][0][j], res["1"][0][j])                  # O
+        assert torch.equal(res["0"][1][j][:, 1:], res["1"][1][j][:, 1:])    # dK, dV
+        torch.testing.assert_close(res["0"][1][j][:, 0].float(), res["1"][1][j][:, 0].float(),
+                                   atol=2e-2, rtol=2e-2)                    # dQ (atomics)
