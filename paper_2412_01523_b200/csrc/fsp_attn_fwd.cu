@@ -40,7 +40,6 @@ struct FwdParams {
   int32_t n_tiles;  // schedule entries (the persistent pair kernel walks them)
   ScatterDev sc;  // fused head->seq of O (sc.degree == 0: off)
   int32_t noncausal;  // FSP_ATTN_NONCAUSAL: every query row sees every key row (pair kernel)
-  int32_t early_qk;   // persistent pair kernel: next entry's first QK_A^T in this entry's last step
 };
 
 template <int D>
@@ -331,7 +330,7 @@ struct Fwd2Smem {
   static constexpr int kK = 2 * kTileBytes;
   static constexpr int kV = kK + kKStages * kTileBytes;  // 2 stages
   static constexpr int kBar = kV + 2 * kTileBytes;
-  static constexpr int kBytes = kBar + 512;
+  static constexpr int kBytes = kBar + 256;
 };
 
 // 2^x on the FMA pipe (x <= 0, finite): round-to-nearest split via the 1.5*2^23 magic
@@ -450,8 +449,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* bar_qa = bars + 0;   // Q_A landed
-  uint64_t* bar_qb = bars + 31;  // Q_B landed (entries with a tile B)
+  uint64_t* bar_q = bars + 0;
   uint64_t* k_full = bars + 1;   // [3]
   uint64_t* k_empty = bars + 4;  // [3]
   uint64_t* v_full = bars + 7;   // [2]
@@ -459,8 +457,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   uint64_t* s_full = bars + 11;  // [2] per tile
   uint64_t* o_done = bars + 13;  // [2] per tile
   uint64_t* p_half = bars + 15;  // [2 tiles][2 halves]: P columns for kv rows 0-63 / 64-127
-  uint64_t* q_empty_a = bars + 19;  // Q_A read by the entry's last QK_A^T
-  uint64_t* q_empty_b = bars + 32;  // Q_B read by the entry's last QK_B^T
+  uint64_t* q_empty = bars + 19; // Q_A / Q_B read by the last QK^T of a schedule entry
   const EntryRing ring{reinterpret_cast<int*>(bars + 24), bars + 20, bars + 22, bars + 26,
                        bars + 25};
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
@@ -474,9 +471,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   // below is a running count of completions, so a wait's parity is (count & 1).
 
   if (threadIdx.x == 0) {
-    mbar_init(q_empty_a, 1);
-    mbar_init(q_empty_b, 1);
-    mbar_init(bar_qb, 1);
+    mbar_init(q_empty, 1);
     mbar_init(epi_free + 0, 4);
     mbar_init(epi_free + 1, 4);
     for (int i = 0; i < 2; ++i) {
@@ -484,7 +479,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       mbar_init(ring.empty + i, kRingConsumers);
     }
     mbar_init(ring.clc, 1);
-    mbar_init(bar_qa, 1);
+    mbar_init(bar_q, 1);
     for (int i = 0; i < L::kKStages; ++i) {
       mbar_init(k_full + i, 1);
       mbar_init(k_empty + i, 1);
@@ -537,16 +532,21 @@ __global__ void __launch_bounds__(kF2Threads, 1)
               tma_prefetch_l2_3d(&tm_k, b * 64, T.head, T.seq_start);
               tma_prefetch_l2_3d(&tm_v, b * 64, T.head, T.seq_start);
             }
-            mbar_wait(q_empty_a, (k - 1) & 1);  // previous entry's QK_A^T MMAs are done
-            // fused head->seq: the previous entry's epilogue stages O in the Q buffers
-            if (p.sc.degree) mbar_wait(epi_free + 0, (k - 1) & 1);
+            mbar_wait(q_empty, (k - 1) & 1);  // previous entry's QK^T MMAs are done
+            if (p.sc.degree) {
+              // fused head->seq: the previous entry's epilogue stages O in the Q buffers
+              mbar_wait(epi_free + 0, (k - 1) & 1);
+              if (wait_b) mbar_wait(epi_free + 1, b_phase);
+            }
           }
-          mbar_expect_tx(bar_qa, L::kTileBytes);
-          for (int b = 0; b < 2; ++b)
-            tma_load_3d(smem + L::kQA + b * 16384, &tm_q, bar_qa, b * 64, T.head, T.seq_start + T.q0);
-          // issue order Q_A, K_0, Q_B, K_1, V_0, K_2, V_1, ...: K is consumed one step before
-          // V, and Q_A / K_0 go first so the next entry's QK_A^T(0) may run in this entry's
-          // last kv step (Q_B is free only after the previous entry's last QK_B^T)
+          mbar_expect_tx(bar_q, (T.has_b ? 2 : 1) * L::kTileBytes);
+          for (int b = 0; b < 2; ++b) {
+            tma_load_3d(smem + L::kQA + b * 16384, &tm_q, bar_q, b * 64, T.head, T.seq_start + T.q0);
+            if (T.has_b)
+              tma_load_3d(smem + L::kQB + b * 16384, &tm_q, bar_q, b * 64, T.head,
+                          T.seq_start + T.q0 + 128);
+          }
+          // issue order K_0, K_1, V_0, K_2, V_1, ...: K is consumed one step before V
           auto load_k = [&](int j) {
             const uint32_t g = g0 + j;
             const int st = g % L::kKStages;
@@ -557,16 +557,6 @@ __global__ void __launch_bounds__(kF2Threads, 1)
                           T.head, T.seq_start + j * 128);
           };
           load_k(0);
-          if (k > 0 && wait_b) {
-            mbar_wait(q_empty_b, b_phase);
-            if (p.sc.degree) mbar_wait(epi_free + 1, b_phase);
-          }
-          if (T.has_b) {
-            mbar_expect_tx(bar_qb, L::kTileBytes);
-            for (int b = 0; b < 2; ++b)
-              tma_load_3d(smem + L::kQB + b * 16384, &tm_q, bar_qb, b * 64, T.head,
-                          T.seq_start + T.q0 + 128);
-          }
           for (int j = 0; j < T.n_kv; ++j) {
             if (j + 1 < T.n_kv) load_k(j + 1);
             const uint32_t g = g0 + j;
@@ -595,26 +585,15 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 #endif
         uint32_t g0 = 0;                 // K/V ring position (kv steps consumed so far)
         uint32_t p_cnt[2] = {0u, 0u};    // p_half completions consumed per tile x
-        uint32_t nb_cnt = 0;             // entries with a tile B so far (bar_qb phases)
         int steps = 0;
-        // Early start of the next entry (persistent launches, p.early_qk): in this entry's
-        // last kv step — after PV_A has consumed P_A for the last time, before the last PV_B
-        // waits for its P — the next entry's QK_A^T(0) is issued if its entry, Q_A and K_0
-        // are already there (non-blocking tests; otherwise it is issued at the entry start as
-        // usual).  Tile A's softmax then starts the next entry while tile B finishes this one,
-        // so the tensor core does not drain at entry boundaries.  Issue order is all that
-        // changes: the results are bit-identical.
-        int w_next = -1;                 // next entry, already taken from the ring
-        bool a0_done = false;            // ... and its QK_A^T(0) already issued
         for (int k = 0;; ++k) {
-          const int w = w_next >= 0 ? w_next : take_entry<kPersistent, false>(ring, k);
-          w_next = -1;
+          const int w = take_entry<kPersistent, false>(ring, k);
           if (w >= p.n_tiles) break;
           const PairTile T = decode_pair(p, w);
           const int n_a = T.n_a, n_b = T.n_b, n_kv = T.n_kv;
-          // S_x = Q_x K_j^T (j counts from this entry's first kv step; j == n_kv is the next
-          // entry's K_0); `last` = this is tile x's last QK^T, which frees Q_x
-          auto qk = [&](int x, int j, bool last) {
+          int qk_left = n_a + n_b;  // QK^T groups still to issue; the last one frees Q_A / Q_B
+          FSP_FTW(5, mbar_wait(bar_q, k & 1));
+          auto qk = [&](int x, int j) {  // S_x = Q_x K_j^T
             const uint32_t qbase = x ? qb : qa;
             const uint32_t kb = k_base + ((g0 + j) % L::kKStages) * L::kTileBytes;
 #pragma unroll
@@ -624,7 +603,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
                      make_sdesc_sw128(kb + off, 16, 1024), idesc_s, kk > 0);
             }
             tc_commit(s_full + x);
-            if (last) tc_commit(x ? q_empty_b : q_empty_a);
+            if (--qk_left == 0) tc_commit(q_empty);
           };
           auto pv = [&](int x, int j) {  // O_x += P_x V_j, each half as soon as its P lands
             const uint32_t vb = v_base + ((g0 + j) & 1) * L::kTileBytes;
@@ -644,17 +623,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
             FSP_FTW(2, mbar_wait(k_full + g % L::kKStages, (g / L::kKStages) & 1));
             tc_fence_after();
           };
-          if (!a0_done) {
-            FSP_FTW(5, mbar_wait(bar_qa, k & 1));
-            wait_k(0);
-            qk(0, 0, n_a == 1);
-          }
-          a0_done = false;
-          if (n_b > 0) {
-            FSP_FTW(5, mbar_wait(bar_qb, nb_cnt & 1));
-            ++nb_cnt;
-            qk(1, 0, n_b == 1);
-          }
+          wait_k(0);
+          qk(0, 0);
+          if (n_b > 0) qk(1, 0);
           tc_commit(k_empty + g0 % L::kKStages);
           for (int j = 0; j < n_kv; ++j) {
             const uint32_t g = g0 + j;
@@ -665,29 +636,16 @@ __global__ void __launch_bounds__(kF2Threads, 1)
               pv(0, j);
               if (j + 1 < n_a) {
                 wait_k(j + 1);
-                qk(0, j + 1, j + 2 == n_a);
+                qk(0, j + 1);
               } else {
                 tc_commit(o_done + 0);
-              }
-            }
-            if (kPersistent && p.early_qk && !next) {
-              const int slot = (k + 1) & 1;
-              const uint32_t gn = g0 + n_kv;  // the next entry's K_0
-              if (mbar_test_wait(ring.full + slot, ((k + 1) >> 1) & 1)) {
-                w_next = take_entry<kPersistent, false>(ring, k + 1);
-                if (w_next < p.n_tiles && mbar_test_wait(bar_qa, (k + 1) & 1) &&
-                    mbar_test_wait(k_full + gn % L::kKStages, (gn / L::kKStages) & 1)) {
-                  tc_fence_after();
-                  qk(0, n_kv, decode_pair(p, w_next).n_a == 1);
-                  a0_done = true;
-                }
               }
             }
             if (j < n_b) {
               pv(1, j);
               if (j + 1 < n_b) {
                 wait_k(j + 1);
-                qk(1, j + 1, j + 2 == n_b);
+                qk(1, j + 1);
               } else {
                 tc_commit(o_done + 1);
               }
@@ -749,7 +707,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       mbar_wait(s_full + x, (s_cnt + j) & 1);
 #if FSP_FWD_TIMING
       const long long ts1 = clock64();
-      if (warp == 2 && lane == 0) atomicAdd(&g_fwd_wait[9], (unsigned long long)(ts1 - ts0));
+      if (warp == kF2SoftmaxWarp0 && lane == 0) atomicAdd(&g_fwd_wait[9], (unsigned long long)(ts1 - ts0));
 #endif
       tc_fence_after();
       if (FSP_ABLATE_EXP >= 2) {  // profiling ablations: 2 = no softmax work,
@@ -833,7 +791,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         }
         const float mx = fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3]));
 #if FSP_FWD_TIMING
-        if (warp == 2 && lane == 0) atomicAdd(&g_fwd_wait[11], (unsigned long long)(clock64() - ts1));
+        if (warp == kF2SoftmaxWarp0 && lane == 0) atomicAdd(&g_fwd_wait[11], (unsigned long long)(clock64() - ts1));
 #endif
         const float m_new = fmaxf(m, mx * sl2);
         // warp-uniform lazy rescale decision (TMEM access is warp-collective)
@@ -906,7 +864,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(p_half + 2 * x);
 #if FSP_FWD_TIMING
-            if (warp == 2 && lane == 0)
+            if (warp == kF2SoftmaxWarp0 && lane == 0)
               atomicAdd(&g_fwd_wait[12], (unsigned long long)(clock64() - ts1));
 #endif
           }
@@ -927,7 +885,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p_half + 2 * x + 1);
 #if FSP_FWD_TIMING
-      if (warp == 2 && lane == 0) atomicAdd(&g_fwd_wait[10], (unsigned long long)(clock64() - ts1));
+      if (warp == kF2SoftmaxWarp0 && lane == 0) atomicAdd(&g_fwd_wait[10], (unsigned long long)(clock64() - ts1));
 #endif
     }
     s_cnt += n_x;
@@ -1030,7 +988,7 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   if ((rc = make_head_tmap(&tq, a->q, a->q_stride, a->n_heads, D, a->total_rows, 128))) return rc;
   if ((rc = make_head_tmap(&tk, a->k, a->k_stride, a->n_heads, D, a->total_rows, 128))) return rc;
   if ((rc = make_head_tmap(&tv, a->v, a->v_stride, a->n_heads, D, a->total_rows, 128))) return rc;
-  FwdParams p{};
+  FwdParams p;
   p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
   p.lse = a->lse;
   p.o_stride = a->o_stride;
@@ -1046,14 +1004,10 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   if (D == 128) {  // schedule entries are 256-row tile pairs (fsp_attn_schedule, head_dim 128)
     const int smem = Fwd2Smem::kBytes + 1024;
     // Persistent launch (CTAs steal not-yet-launched entries, so an entry's Q load and first
-    // QK^T overlap the previous entry's softmax tail and epilogue); FSP_FWD_PERSISTENT=0
-    // launches one CTA per entry.  FSP_FWD_EARLY=0 keeps every entry's first QK^T at its
-    // start (A/B switch of the early start; it is skipped while the head->seq exchange is
-    // fused, whose epilogue stages O in the Q buffer the early QK_A^T would need).
+    // QK^T overlap the previous entry's softmax tail and epilogue) unless the head->seq
+    // exchange is fused, whose epilogue stages rows in the entry's Q buffer.
     const char* env = getenv("FSP_FWD_PERSISTENT");
     const bool persistent = !(env && env[0] == '0');
-    const char* env_early = getenv("FSP_FWD_EARLY");
-    p.early_qk = (p.sc.degree == 0 && !(env_early && env_early[0] == '0')) ? 1 : 0;
     if (persistent) {
       FSP_CUDA(cudaFuncSetAttribute(attn_fwd_pair_kernel<true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
