@@ -34,8 +34,9 @@ VIRTUAL_ONLY = [
     # a 9-token sequence at d = 8 (members holding only pad rows) and empty selected groups
     (8, "tiny_n8.json", 8, 128),
     (8, "rand1_n8_flexsp.json", 4, 64)]
-FULLSIZE = [(4, "c2_n4_flexsp.json", 32, 128), (8, "c2_n8_static.json", 32, 128),
-            (8, "c4_n8_flexsp.json", 52, 128)]
+# the C2 plans the N=4 / N=8 bench lines run ([2,1,1]; [4,1,1,1,1]; static d=8) and C4 at d=8
+FULLSIZE = [(4, "c2_n4_flexsp.json", 32, 128), (8, "c2_n8_flexsp.json", 32, 128),
+            (8, "c2_n8_static.json", 32, 128), (8, "c4_n8_flexsp.json", 52, 128)]
 
 
 def _release_gpu_memory():
