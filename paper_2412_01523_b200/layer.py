@@ -9,9 +9,9 @@ Under a FlexSP plan the "shard" of a rank is its loader-order rows of the micro-
 
 `FlexSPTransformerLayer` is that pre-LayerNorm GPT block (LN -> QKV -> SP attention -> O
 -> residual, LN -> MLP(GELU) -> residual) in bf16.  The GEMMs are cuBLAS through torch
-(plain library GEMMs — the hot path this repo owns is the SP attention step); weights are
-replicated on every rank, and their cross-rank gradient reduction (FSDP / ZeRO, §8f rank 4)
-is out of scope.  This turns the attention-layer step into the per-layer cost of a full
+(plain library GEMMs — the hot path this repo owns is the SP attention step); the layer
+holds ordinary parameters, which `zero.ZeroStack` shards ZeRO-3 style across the world
+(§8f rank 4; scripts/bench_full_step.py) or which stay replicated.  This turns the attention-layer step into the per-layer cost of a full
 forward/backward step, where the token-linear terms (α2 of the planner's cost model,
 pkg/src/seqplan/cost_model.py:5-7) sit beside the quadratic attention term.
 """
