@@ -24,6 +24,7 @@ B200 design:
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Any, Sequence
 
@@ -143,6 +144,9 @@ class FlexSPExecutor:
         # backward go straight to their owners' sequence shards); False = separate
         # fsp_a2a_head2seq launches after attention (kept for A/B measurements)
         self.fuse_head2seq = fuse_head2seq
+        # step(): the attention forward clears the backward's fp32 dQ accumulator (ABI 7,
+        # FSP_ATTN_DQ_ZEROED); FSP_ZERO_DQ_IN_FWD=0 leaves it to the backward (A/B switch)
+        self.zero_dq_in_fwd = os.environ.get("FSP_ZERO_DQ_IN_FWD", "1") != "0"
         # heap_factory(nbytes) -> PeerHeap-like (view / peer / nbytes); None = the
         # symmetric-memory heap.  vranks.VirtualCluster passes per-virtual-rank heaps that
         # live on one device (the single-GPU multi-rank harness).
@@ -431,8 +435,9 @@ class FlexSPExecutor:
         """fwd+bwd of every micro-batch in plan order.  `sink(m, out, dqkv)` consumes the
         outputs before the next micro-batch reuses the heap regions (e.g. a copy-out)."""
         for m, mb in enumerate(sp.micro_batches):
-            out, saved = self.micro_batch_forward(sp, mb, qkv_locals[m], zero_dq=True)
-            dqkv = self.micro_batch_backward(sp, mb, saved, dout_locals[m], dq_zeroed=True)
+            z = self.zero_dq_in_fwd
+            out, saved = self.micro_batch_forward(sp, mb, qkv_locals[m], zero_dq=z)
+            dqkv = self.micro_batch_backward(sp, mb, saved, dout_locals[m], dq_zeroed=z)
             if sink is not None:
                 sink(m, out, dqkv)
 
@@ -511,9 +516,9 @@ class FlexSPExecutor:
             d = self.heap.view(off["in_do"], (mb.n_local, self.n_heads, self.head_dim),
                                torch.bfloat16)
             self._wait_out_slot(cur, "out")
-            out, saved = self.micro_batch_forward(sp, mb, q, zero_dq=True)
+            out, saved = self.micro_batch_forward(sp, mb, q, zero_dq=self.zero_dq_in_fwd)
             self._wait_out_slot(cur, "dqkv")
-            dqkv = self.micro_batch_backward(sp, mb, saved, d, dq_zeroed=True)
+            dqkv = self.micro_batch_backward(sp, mb, saved, d, dq_zeroed=self.zero_dq_in_fwd)
             if sink is not None:
                 sink(m, out, dqkv)
             self._copy_out(cur, m, out, dqkv, mb.n_local, host_out, host_dqkv)
@@ -641,9 +646,9 @@ class FlexSPExecutor:
             d = bufs[k][1][:rows * hd].view(rows, self.n_heads, self.head_dim)
             # the output slots this micro-batch writes must have been copied out already
             self._wait_out_slot(cur, "out")
-            out, saved = self.micro_batch_forward(sp, mb, q, zero_dq=True)
+            out, saved = self.micro_batch_forward(sp, mb, q, zero_dq=self.zero_dq_in_fwd)
             self._wait_out_slot(cur, "dqkv")
-            dqkv = self.micro_batch_backward(sp, mb, saved, d, dq_zeroed=True)
+            dqkv = self.micro_batch_backward(sp, mb, saved, d, dq_zeroed=self.zero_dq_in_fwd)
             if sink is not None:
                 sink(m, out, dqkv)
             consumed[k].record(cur)

@@ -278,6 +278,7 @@ def test_forward_clears_the_dq_accumulator(persistent, monkeypatch):
     """ABI 7: attn_fwd(dq_zero=) zero-fills the next backward's fp32 dQ accumulator with the
     forward's idle warps (a slice per schedule entry, whichever CTA runs it), and
     attn_bwd(dq_zeroed=True) then skips that pass — bit-identical dQ / dK / dV."""
+    ops = _ops()
     monkeypatch.setenv("FSP_FWD_PERSISTENT", persistent)
     H, D = 4, 128
     lengths = [1, 77, 128, 129, 300, 1000, 2048] * 20
