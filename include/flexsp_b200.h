@@ -41,13 +41,10 @@ extern "C" {
 #define FSP_ERR_CUDA (-2)
 #define FSP_ERR_UNSUPPORTED (-3)
 
-#define FSP_ABI_VERSION 7
+#define FSP_ABI_VERSION 6
 
 /* FspAttnFwd / FspAttnBwd .flags */
 #define FSP_ATTN_NONCAUSAL 1
-/* FspAttnBwd .flags (ABI 7): dq_accum is already zero (a preceding fsp_attn_fwd cleared it
- * through FspAttnFwd.dq_zero), so the backward's first pass only computes delta */
-#define FSP_ATTN_DQ_ZEROED 2
 
 int fsp_abi_version(void);
 const char* fsp_last_error(void);
@@ -179,11 +176,6 @@ typedef struct FspAttnFwd {
   int32_t flags;          /* ABI 6: FSP_ATTN_NONCAUSAL = every query row of a sequence sees
                              every key row of it (a context-parallel block whose keys all
                              precede its queries); 0 = causal */
-  void* dq_zero;          /* ABI 7: optional buffer the forward zero-fills while it computes
-                             (the next backward's dq_accum: the forward is compute-bound and
-                             leaves HBM bandwidth idle; pass FSP_ATTN_DQ_ZEROED to that
-                             backward); NULL = none.  16-byte aligned */
-  int64_t dq_zero_bytes;  /* multiple of 16 */
 } FspAttnFwd;
 
 typedef struct FspAttnBwd {
@@ -209,8 +201,7 @@ typedef struct FspAttnBwd {
   int32_t head_dim;
   float softmax_scale;
   FspHeadScatter scatter; /* ABI 4: optional fused head->seq of dQ/dK/dV (degree 0 = off) */
-  int32_t flags;          /* ABI 6: FSP_ATTN_NONCAUSAL (as in FspAttnFwd); ABI 7:
-                             FSP_ATTN_DQ_ZEROED */
+  int32_t flags;          /* ABI 6: FSP_ATTN_NONCAUSAL (as in FspAttnFwd) */
 } FspAttnBwd;
 
 /* CTA schedule: writes n entries of two int32 {seq << 16 | unit, head} to tiles_host

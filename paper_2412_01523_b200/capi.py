@@ -17,9 +17,8 @@ FSP_OK = 0
 FSP_ERR_INVALID = -1
 FSP_ERR_CUDA = -2
 FSP_ERR_UNSUPPORTED = -3
-ABI_VERSION = 7
+ABI_VERSION = 6
 FSP_ATTN_NONCAUSAL = 1
-FSP_ATTN_DQ_ZEROED = 2
 FSP_SCHED_FWD = 0
 FSP_SCHED_BWD = 1
 
@@ -56,8 +55,7 @@ class FspAttnFwd(ctypes.Structure):
                 ("o_stride", c_i64), ("d_cu_seqlens", c_vp), ("d_seq_starts", c_vp),
                 ("d_tiles", c_vp), ("n_tiles", c_i32), ("n_seq", c_i32), ("total_rows", c_i32),
                 ("n_heads", c_i32), ("head_dim", c_i32), ("softmax_scale", c_float),
-                ("scatter", FspHeadScatter), ("flags", c_i32),
-                ("dq_zero", c_vp), ("dq_zero_bytes", c_i64)]
+                ("scatter", FspHeadScatter), ("flags", c_i32)]
 
 
 class FspAttnBwd(ctypes.Structure):

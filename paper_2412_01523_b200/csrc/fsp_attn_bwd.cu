@@ -335,7 +335,7 @@ template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(
     const __nv_bfloat16* __restrict__ o, int64_t o_stride, const __nv_bfloat16* __restrict__ dout,
     int64_t do_stride, float* __restrict__ delta, float* __restrict__ dq_accum, int total_rows,
-    int n_heads, bool zero_dq) {
+    int n_heads) {
   constexpr int kPer = D / 32;  // elements per lane (2 or 4)
   const int64_t n = (int64_t)total_rows * n_heads;
   const int lane = threadIdx.x & 31;
@@ -365,7 +365,6 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
     if (lane == 0) delta[(int64_t)h * total_rows + t] = acc;
-    if (!zero_dq) continue;  // FSP_ATTN_DQ_ZEROED: the forward cleared dq_accum
     float* dq = dq_accum + ((int64_t)h * total_rows + t) * D + lane * kPer;
     if (kPer == 4)
       *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1155,8 +1154,7 @@ int launch_bwd(const FspAttnBwd* a, cudaStream_t stream) {
     if (blocks > 148 * 8) blocks = 148 * 8;
     attn_bwd_prep_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(a->o), a->o_stride,
-        reinterpret_cast<const __nv_bfloat16*>(a->dout), a->do_stride, a->delta, a->dq_accum, T, H,
-        !(a->flags & FSP_ATTN_DQ_ZEROED));
+        reinterpret_cast<const __nv_bfloat16*>(a->dout), a->do_stride, a->delta, a->dq_accum, T, H);
     FSP_LAUNCH_CHECK();
   }
   if (a->n_tiles > 0) {
@@ -1234,8 +1232,7 @@ extern "C" int fsp_attn_bwd(const FspAttnBwd* a, void* stream) {
                 a->head_dim);
   FSP_CHECK_ARG(a->n_heads >= 1, "n_heads must be >= 1");
   FSP_CHECK_ARG(a->total_rows >= 0 && a->n_tiles >= 0, "negative sizes");
-  FSP_CHECK_ARG((a->flags & ~(FSP_ATTN_NONCAUSAL | FSP_ATTN_DQ_ZEROED)) == 0,
-                "unknown attention flags 0x%x", a->flags);
+  FSP_CHECK_ARG((a->flags & ~FSP_ATTN_NONCAUSAL) == 0, "unknown attention flags 0x%x", a->flags);
   FSP_CHECK_ARG(!(a->flags & FSP_ATTN_NONCAUSAL) || a->head_dim == 128,
                 "FSP_ATTN_NONCAUSAL needs head_dim 128");
   if (a->total_rows == 0 && a->n_tiles == 0) return FSP_OK;  // empty group: no-op

@@ -40,8 +40,6 @@ struct FwdParams {
   int32_t n_tiles;  // schedule entries (the persistent pair kernel walks them)
   ScatterDev sc;  // fused head->seq of O (sc.degree == 0: off)
   int32_t noncausal;  // FSP_ATTN_NONCAUSAL: every query row sees every key row (pair kernel)
-  uint4* zero;        // ABI 7 dq_zero: cleared by the idle warps, a slice per schedule entry
-  int64_t zero_n16;   // ... in 16-byte units
 };
 
 template <int D>
@@ -406,7 +404,7 @@ struct EntryRing {
   void* resp;       // 16-byte cluster-launch-control response
   uint64_t* clc;    // its completion barrier
 };
-constexpr int kRingConsumers = 9 + (FSP_FWD_WG3 ? 2 : 0);  // MMA thread + softmax warps (+ zeroing warps)
+constexpr int kRingConsumers = 9;
 
 // Producer side: the k-th entry of this CTA (its own first, then stolen ones).
 template <bool kPersistent>
@@ -679,20 +677,6 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 #endif
       }
       __syncwarp();
-    } else {
-      // ------------------------------------------------------------ warps 2, 3 (WG3 only)
-      // Clear p.zero (the next backward's fp32 dQ accumulator, FSP_ATTN_DQ_ZEROED) while the
-      // tensor core and softmax run: schedule entry w clears slice w of it, so whichever CTA
-      // runs an entry clears its slice exactly once.  HBM is nearly idle in this
-      // compute-bound kernel; the prep pass of the backward then only computes delta.
-      const int zt = ((int)warp - 2) * 32 + (int)lane;  // 0..63
-      for (int k = 0;; ++k) {
-        const int w = take_entry<kPersistent, true>(ring, k);
-        if (w >= p.n_tiles) break;
-        if (p.zero == nullptr) continue;
-        const int64_t b = p.zero_n16 * w / p.n_tiles, e = p.zero_n16 * (w + 1) / p.n_tiles;
-        for (int64_t i = b + zt; i < e; i += 64) p.zero[i] = make_uint4(0u, 0u, 0u, 0u);
-      }
     }
   } else {
 #if FSP_FWD_WG3
@@ -1004,7 +988,7 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   if ((rc = make_head_tmap(&tq, a->q, a->q_stride, a->n_heads, D, a->total_rows, 128))) return rc;
   if ((rc = make_head_tmap(&tk, a->k, a->k_stride, a->n_heads, D, a->total_rows, 128))) return rc;
   if ((rc = make_head_tmap(&tv, a->v, a->v_stride, a->n_heads, D, a->total_rows, 128))) return rc;
-  FwdParams p{};
+  FwdParams p;
   p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
   p.lse = a->lse;
   p.o_stride = a->o_stride;
@@ -1017,19 +1001,11 @@ static int launch_fwd(const FspAttnFwd* a, cudaStream_t stream) {
   if ((rc = scatter_from_abi(a->scatter, 1, a->n_heads, D, a->total_rows, &p.sc))) return rc;
   p.n_tiles = a->n_tiles;
   p.noncausal = (a->flags & FSP_ATTN_NONCAUSAL) ? 1 : 0;
-  // dq_zero: cleared inside the pair kernel (its two idle warps), else by a memset
-  const bool zero_in_kernel = a->dq_zero && D == 128 && FSP_FWD_WG3 && a->n_tiles > 0;
-  if (a->dq_zero && !zero_in_kernel && a->dq_zero_bytes)
-    FSP_CUDA(cudaMemsetAsync(a->dq_zero, 0, (size_t)a->dq_zero_bytes, stream));
-  if (zero_in_kernel) {
-    p.zero = reinterpret_cast<uint4*>(a->dq_zero);
-    p.zero_n16 = a->dq_zero_bytes / 16;
-  }
   if (D == 128) {  // schedule entries are 256-row tile pairs (fsp_attn_schedule, head_dim 128)
     const int smem = Fwd2Smem::kBytes + 1024;
     // Persistent launch (CTAs steal not-yet-launched entries, so an entry's Q load and first
-    // QK^T overlap the previous entry's softmax tail and epilogue); FSP_FWD_PERSISTENT=0
-    // launches one CTA per entry.
+    // QK^T overlap the previous entry's softmax tail and epilogue) unless the head->seq
+    // exchange is fused, whose epilogue stages rows in the entry's Q buffer.
     const char* env = getenv("FSP_FWD_PERSISTENT");
     const bool persistent = !(env && env[0] == '0');
     if (persistent) {
@@ -1131,16 +1107,7 @@ extern "C" int fsp_attn_fwd(const FspAttnFwd* a, void* stream) {
   FSP_CHECK_ARG((a->flags & ~FSP_ATTN_NONCAUSAL) == 0, "unknown attention flags 0x%x", a->flags);
   FSP_CHECK_ARG(!(a->flags & FSP_ATTN_NONCAUSAL) || a->head_dim == 128,
                 "FSP_ATTN_NONCAUSAL needs head_dim 128");
-  FSP_CHECK_ARG(a->dq_zero_bytes >= 0 && a->dq_zero_bytes % 16 == 0 &&
-                    reinterpret_cast<uintptr_t>(a->dq_zero) % 16 == 0 &&
-                    (a->dq_zero != nullptr || a->dq_zero_bytes == 0),
-                "dq_zero must be 16-byte aligned with a size that is a multiple of 16");
-  if (a->total_rows == 0 && a->n_tiles == 0) {
-    if (a->dq_zero && a->dq_zero_bytes)
-      FSP_CUDA(cudaMemsetAsync(a->dq_zero, 0, (size_t)a->dq_zero_bytes,
-                               static_cast<cudaStream_t>(stream)));
-    return FSP_OK;
-  }
+  if (a->total_rows == 0 && a->n_tiles == 0) return FSP_OK;
   int rc = check_attn_common(a->q, a->k, a->v, a->q_stride, a->k_stride, a->v_stride,
                              a->d_cu_seqlens, a->d_tiles, a->n_tiles, a->n_seq, a->total_rows,
                              a->n_heads, a->head_dim);

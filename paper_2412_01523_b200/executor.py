@@ -24,7 +24,6 @@ B200 design:
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass, field
 from typing import Any, Sequence
 
@@ -144,9 +143,6 @@ class FlexSPExecutor:
         # backward go straight to their owners' sequence shards); False = separate
         # fsp_a2a_head2seq launches after attention (kept for A/B measurements)
         self.fuse_head2seq = fuse_head2seq
-        # step(): the attention forward clears the backward's fp32 dQ accumulator (ABI 7,
-        # FSP_ATTN_DQ_ZEROED); FSP_ZERO_DQ_IN_FWD=0 leaves it to the backward (A/B switch)
-        self.zero_dq_in_fwd = os.environ.get("FSP_ZERO_DQ_IN_FWD", "1") != "0"
         # heap_factory(nbytes) -> PeerHeap-like (view / peer / nbytes); None = the
         # symmetric-memory heap.  vranks.VirtualCluster passes per-virtual-rank heaps that
         # live on one device (the single-GPU multi-rank harness).
@@ -284,14 +280,10 @@ class FlexSPExecutor:
                               torch.bfloat16)
         return out, dqkv
 
-    def micro_batch_forward(self, sp: StepPlan, mb: RankMicroBatch, qkv_local: torch.Tensor,
-                            zero_dq: bool = False):
+    def micro_batch_forward(self, sp: StepPlan, mb: RankMicroBatch, qkv_local: torch.Tensor):
         """Eq. (2)-(4) forward on this rank.  qkv_local: [n_local, 3, H, D] bf16.
 
         Returns (out_local view [n_local, H, D], saved) where saved feeds the backward.
-        zero_dq: the attention forward also clears the backward's fp32 dQ accumulator (the
-        backward of this micro-batch must follow with dq_zeroed=True, nothing in between
-        using the executor's workspaces — as in step()).
         """
         # Entry barrier over this micro-batch's group only: its members are about to write
         # into each other's heap regions, so every member must be done (in stream order)
@@ -314,11 +306,9 @@ class FlexSPExecutor:
             for _ in range(2):  # keep the barrier epochs in step with the exchanging ranks
                 self._next_epoch()
             out_local, _ = self.local_buffers(sp, mb)
-            dq_zero = (self._workspace("dq_accum", mb.n_local * H * D, torch.float32)
-                       if zero_dq else None)
             with self.timer.span("attn_fwd", mb.fwd_flops):
                 _, lse = ops.attn_fwd(qkv_local[:, 0], qkv_local[:, 1], qkv_local[:, 2], mb.sched,
-                                      self.scale, out=out_local, dq_zero=dq_zero)
+                                      self.scale, out=out_local)
             return out_local, (qkv_local, out_local, lse)
         self._barrier(ranks, ep_entry, "entry_barrier")
         off = sp.offsets
@@ -337,11 +327,9 @@ class FlexSPExecutor:
         if self.fuse_head2seq:  # Eq. (4) inside the attention epilogue
             scatter = ops.HeadScatter(d, R, hb[j], H * D, 0, mb.unpack_table,
                                       [self.heap.peer(r, self._out_off(sp)) for r in ranks])
-        dq_zero = self._workspace("dq_accum", T * hn * D, torch.float32) if zero_dq else None
         with self.timer.span("attn_fwd", mb.fwd_flops):
             _, lse = ops.attn_fwd(recv[:, 0, :hn], recv[:, 1, :hn], recv[:, 2, :hn], mb.sched,
-                                  self.scale, out=o_heads[:, :hn], scatter=scatter,
-                                  dq_zero=dq_zero)
+                                  self.scale, out=o_heads[:, :hn], scatter=scatter)
         if scatter is not None:
             self.timer.count("head2seq_fused", sent_out)  # NVLink bytes inside attn_fwd
             self._barrier(ranks, self._next_epoch(), "fused_barrier")
@@ -363,10 +351,8 @@ class FlexSPExecutor:
                 rows_per_rank=R, n_mats=3, n_heads=H, head_dim=D, dst_stride=3 * hm * D,
                 index=mb.pack_index, head_begin=mb.head_begin)
 
-    def micro_batch_backward(self, sp: StepPlan, mb: RankMicroBatch, saved, dout_local: torch.Tensor,
-                             dq_zeroed: bool = False):
-        """Backward of micro_batch_forward: dout_local [n_local, H, D] -> dqkv_local view.
-        dq_zeroed: the forward ran with zero_dq=True."""
+    def micro_batch_backward(self, sp: StepPlan, mb: RankMicroBatch, saved, dout_local: torch.Tensor):
+        """Backward of micro_batch_forward: dout_local [n_local, H, D] -> dqkv_local view."""
         ep_entry = self._next_epoch()  # group entry barrier, as in the forward
         self._n_bwd += 1
         grp = mb.group
@@ -386,7 +372,7 @@ class FlexSPExecutor:
             with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
                 ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, dout_local, lse,
                              mb.sched, self.scale, dq=dqkv_local[:, 0], dk=dqkv_local[:, 1],
-                             dv=dqkv_local[:, 2], dq_accum=dq_acc, delta=delta, dq_zeroed=dq_zeroed)
+                             dv=dqkv_local[:, 2], dq_accum=dq_acc, delta=delta)
             return dqkv_local
         d, j, R = grp.degree, mb.j, grp.rows_per_rank
         hn, hm, hb = mb.n_heads_local, mb.heads_stride, mb.head_begin
@@ -411,8 +397,7 @@ class FlexSPExecutor:
                                       [self.heap.peer(r, self._dqkv_off(sp)) for r in ranks])
             with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
                 ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, do_recv[:, :hn], lse,
-                             mb.sched, self.scale, dq_accum=dq_acc, delta=delta, scatter=scatter,
-                             dq_zeroed=dq_zeroed)
+                             mb.sched, self.scale, dq_accum=dq_acc, delta=delta, scatter=scatter)
             self.timer.count("head2seq_fused", 3 * sent_out)  # NVLink bytes inside attn_bwd
             self._barrier(ranks, self._next_epoch(), "fused_barrier")
             return dqkv_local
@@ -420,7 +405,7 @@ class FlexSPExecutor:
         with self.timer.span("attn_bwd", 2.5 * mb.fwd_flops):
             ops.attn_bwd(recv[:, 0], recv[:, 1], recv[:, 2], o_heads, do_recv[:, :hn], lse,
                          mb.sched, self.scale, dq=dqkv_heads[:, 0, :hn], dk=dqkv_heads[:, 1, :hn],
-                         dv=dqkv_heads[:, 2, :hn], dq_accum=dq_acc, delta=delta, dq_zeroed=dq_zeroed)
+                         dv=dqkv_heads[:, 2, :hn], dq_accum=dq_acc, delta=delta)
         _, dqkv_local = self.local_buffers(sp, mb)
         with self.timer.span("a2a", 3 * sent_out):
             ops.a2a("head2seq", dqkv_heads.view(T, 3 * hm * D),
@@ -435,9 +420,8 @@ class FlexSPExecutor:
         """fwd+bwd of every micro-batch in plan order.  `sink(m, out, dqkv)` consumes the
         outputs before the next micro-batch reuses the heap regions (e.g. a copy-out)."""
         for m, mb in enumerate(sp.micro_batches):
-            z = self.zero_dq_in_fwd
-            out, saved = self.micro_batch_forward(sp, mb, qkv_locals[m], zero_dq=z)
-            dqkv = self.micro_batch_backward(sp, mb, saved, dout_locals[m], dq_zeroed=z)
+            out, saved = self.micro_batch_forward(sp, mb, qkv_locals[m])
+            dqkv = self.micro_batch_backward(sp, mb, saved, dout_locals[m])
             if sink is not None:
                 sink(m, out, dqkv)
 
@@ -516,9 +500,9 @@ class FlexSPExecutor:
             d = self.heap.view(off["in_do"], (mb.n_local, self.n_heads, self.head_dim),
                                torch.bfloat16)
             self._wait_out_slot(cur, "out")
-            out, saved = self.micro_batch_forward(sp, mb, q, zero_dq=self.zero_dq_in_fwd)
+            out, saved = self.micro_batch_forward(sp, mb, q)
             self._wait_out_slot(cur, "dqkv")
-            dqkv = self.micro_batch_backward(sp, mb, saved, d, dq_zeroed=self.zero_dq_in_fwd)
+            dqkv = self.micro_batch_backward(sp, mb, saved, d)
             if sink is not None:
                 sink(m, out, dqkv)
             self._copy_out(cur, m, out, dqkv, mb.n_local, host_out, host_dqkv)
@@ -646,9 +630,9 @@ class FlexSPExecutor:
             d = bufs[k][1][:rows * hd].view(rows, self.n_heads, self.head_dim)
             # the output slots this micro-batch writes must have been copied out already
             self._wait_out_slot(cur, "out")
-            out, saved = self.micro_batch_forward(sp, mb, q, zero_dq=self.zero_dq_in_fwd)
+            out, saved = self.micro_batch_forward(sp, mb, q)
             self._wait_out_slot(cur, "dqkv")
-            dqkv = self.micro_batch_backward(sp, mb, saved, d, dq_zeroed=self.zero_dq_in_fwd)
+            dqkv = self.micro_batch_backward(sp, mb, saved, d)
             if sink is not None:
                 sink(m, out, dqkv)
             consumed[k].record(cur)

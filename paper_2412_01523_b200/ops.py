@@ -175,14 +175,11 @@ def _rows_view_ok(t: torch.Tensor, H: int, D: int) -> None:
 
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSchedule,
              softmax_scale: float | None = None, out: torch.Tensor | None = None,
-             scatter: HeadScatter | None = None, causal: bool = True,
-             dq_zero: torch.Tensor | None = None):
+             scatter: HeadScatter | None = None, causal: bool = True):
     """Varlen causal attention forward; q/k/v [T, H, D] bf16 (row-strided views OK).
     `scatter` fuses the head->seq exchange of O into the epilogue (O is still written
     to `out`).  causal=False (FSP_ATTN_NONCAUSAL, D=128): every query row of a sequence
-    sees every key row of it — a context-parallel block whose keys precede its queries.
-    `dq_zero` (ABI 7): a buffer (the next attn_bwd's dq_accum) this launch zero-fills while
-    it computes; pass dq_zeroed=True to that attn_bwd."""
+    sees every key row of it — a context-parallel block whose keys precede its queries."""
     _require_cuda(q, k, v)
     T, H, D = q.shape
     for t in (q, k, v):
@@ -200,12 +197,6 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
     if scatter is not None:
         a.scatter = scatter.to_c()
     a.flags = 0 if causal else capi.FSP_ATTN_NONCAUSAL
-    if dq_zero is not None:
-        _require_cuda(dq_zero)
-        if not dq_zero.is_contiguous():
-            raise ValueError("dq_zero must be contiguous")
-        a.dq_zero = dq_zero.data_ptr()
-        a.dq_zero_bytes = dq_zero.numel() * dq_zero.element_size()
     capi.check(capi.load().fsp_attn_fwd(ctypes.byref(a), _stream()))
     LAUNCHES[0] += 1 if sched.n_fwd else 0
     return o, lse
@@ -213,14 +204,13 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sched: AttnSched
 
 def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | None = None,
              dq=None, dk=None, dv=None, dq_accum=None, delta=None,
-             scatter: HeadScatter | None = None, causal: bool = True, dq_zeroed: bool = False):
+             scatter: HeadScatter | None = None, causal: bool = True):
     """Varlen causal attention backward -> (dq, dk, dv), each [T, H, D] bf16.
 
     dq_accum (fp32 [H, T, D]) and delta (fp32 [H, T]) are optional reusable workspaces
     (fsp_attn_bwd_workspace_bytes gives their combined size).  With `scatter` the
     head->seq exchange of dQ / dK / dV (destination matrices 0 / 1 / 2) is fused into the
     kernels and nothing is written locally: the result is (None, None, None).
-    dq_zeroed (FSP_ATTN_DQ_ZEROED): dq_accum was cleared by the preceding attn_fwd(dq_zero=).
     """
     _require_cuda(q, k, v, o, dout, lse)
     T, H, D = q.shape
@@ -255,9 +245,7 @@ def attn_bwd(q, k, v, o, dout, lse, sched: AttnSchedule, softmax_scale: float | 
                         sched.n_bwd, sched.n_seq, T, H, D, scale)
     if scatter is not None:
         a.scatter = scatter.to_c()
-    a.flags = (0 if causal else capi.FSP_ATTN_NONCAUSAL) | (capi.FSP_ATTN_DQ_ZEROED if dq_zeroed else 0)
-    if dq_zeroed and dq_accum is None:
-        raise ValueError("dq_zeroed needs the dq_accum workspace the forward cleared")
+    a.flags = 0 if causal else capi.FSP_ATTN_NONCAUSAL
     capi.check(capi.load().fsp_attn_bwd(ctypes.byref(a), _stream()))
     LAUNCHES[0] += (2 if T else 0) + (1 if sched.n_bwd else 0)
     return dq, dk, dv

@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared == set(capi.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.fsp_abi_version() == capi.ABI_VERSION == 7
+    assert lib.fsp_abi_version() == capi.ABI_VERSION == 6
 
 
 def _schedule(lib, lens, rev, heads=1, head_dim=64):
@@ -228,7 +228,7 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
         "FspHeadScatter": ["degree", "head_offset", "dst_stride", "mat_stride", "d_unpack",
                            "peer_dst"],
         "FspAttnFwd": ["q", "lse", "o_stride", "d_seq_starts", "n_tiles", "softmax_scale",
-                       "scatter", "flags", "dq_zero", "dq_zero_bytes"],
+                       "scatter", "flags"],
         "FspAttnBwd": ["dout", "dv", "dv_stride", "dq_accum", "d_tiles", "softmax_scale",
                        "scatter", "flags"],
     }

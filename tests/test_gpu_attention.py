@@ -271,40 +271,3 @@ def test_noncausal_matches_sdpa(lengths, H):
         for got, t in ((dq, qs), (dk, ks), (dv, vs)):
             torch.testing.assert_close(got[a:b].float().cpu().transpose(0, 1), t.grad,
                                        atol=5e-2, rtol=5e-2)
-
-
-@pytest.mark.parametrize("persistent", ["1", "0"])
-def test_forward_clears_the_dq_accumulator(persistent, monkeypatch):
-    """ABI 7: attn_fwd(dq_zero=) zero-fills the next backward's fp32 dQ accumulator with the
-    forward's idle warps (a slice per schedule entry, whichever CTA runs it), and
-    attn_bwd(dq_zeroed=True) then skips that pass — bit-identical dQ / dK / dV."""
-    ops = _ops()
-    monkeypatch.setenv("FSP_FWD_PERSISTENT", persistent)
-    H, D = 4, 128
-    lengths = [1, 77, 128, 129, 300, 1000, 2048] * 20
-    cu = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32)
-    T = int(cu[-1])
-    sched = ops.AttnSchedule.build(cu, "cuda", H, head_dim=D)
-    g = torch.Generator(device="cuda").manual_seed(3)
-    q, k, v, do = (torch.randn((T, H, D), generator=g, device="cuda", dtype=torch.bfloat16)
-                   for _ in range(4))
-    o, lse = ops.attn_fwd(q, k, v, sched)
-    ref = ops.attn_bwd(q, k, v, o, do, lse, sched)
-    acc = torch.full((H, T, D), float("nan"), dtype=torch.float32, device="cuda")
-    delta = torch.empty((H, T), dtype=torch.float32, device="cuda")
-    o2, lse2 = ops.attn_fwd(q, k, v, sched, dq_zero=acc)
-    torch.cuda.synchronize()
-    assert torch.equal(o2, o) and torch.equal(lse2, lse)
-    assert int(torch.count_nonzero(acc)) == 0          # every element cleared (NaN != 0)
-    acc.fill_(float("nan"))
-    ops.attn_fwd(q, k, v, sched, dq_zero=acc)
-    out = ops.attn_bwd(q, k, v, o, do, lse, sched, dq_accum=acc, delta=delta, dq_zeroed=True)
-    for a, b in zip(out, ref):
-        assert torch.equal(a, b)
-    # odd size (a slice boundary inside a row) and the size / alignment checks
-    odd = torch.full((T * 3 + 4,), 7.0, dtype=torch.float32, device="cuda")
-    ops.attn_fwd(q, k, v, sched, dq_zero=odd)
-    torch.cuda.synchronize()
-    assert int(torch.count_nonzero(odd)) == 0
-    with pytest.raises(ValueError):
-        ops.attn_fwd(q, k, v, sched, dq_zero=odd[1:])     # 4-byte aligned, 4-byte multiple
