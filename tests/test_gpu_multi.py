@@ -34,6 +34,9 @@ VIRTUAL_ONLY = [
     # a 9-token sequence at d = 8 (members holding only pad rows) and empty selected groups
     (8, "tiny_n8.json", 8, 128),
     (8, "rand1_n8_flexsp.json", 4, 64)]
+# random batches planned at test time by the reference planner (baseline/_ref), uneven heads
+FUZZ = [(4, "fuzz11_n4", 6, 128), (8, "fuzz12_n8", 10, 128), (4, "fuzz13_n4", 8, 64),
+        (8, "fuzz14_n8", 13, 128)]
 # the C2 plans the N=4 / N=8 bench lines run ([2,1,1]; [4,1,1,1,1]; static d=8) and C4 at d=8
 FULLSIZE = [(4, "c2_n4_flexsp.json", 32, 128), (8, "c2_n8_flexsp.json", 32, 128),
             (8, "c2_n8_static.json", 32, 128), (8, "c4_n8_flexsp.json", 52, 128)]
@@ -78,6 +81,16 @@ def test_mgpu_step_matches_oracle(n, plan, heads, head_dim):
 
 @pytest.mark.parametrize("n,plan,heads,head_dim", VIRTUAL_ONLY)
 def test_virtual_ranks_match_oracle(n, plan, heads, head_dim):
+    _virtual("dense", n, plan, heads, head_dim)
+
+
+@pytest.mark.parametrize("n,plan,heads,head_dim", FUZZ)
+def test_virtual_ranks_random_reference_plans(n, plan, heads, head_dim):
+    try:
+        from paper_2412_01523_b200.planning import import_seqplan
+        import_seqplan()
+    except ImportError:
+        pytest.skip("reference planner not installed (baseline/_ref)")
     _virtual("dense", n, plan, heads, head_dim)
 
 

@@ -60,7 +60,36 @@ def load_plan(name):
                                  {"slot_id": 4, "degree": 2, "sequence_indices": []}]},
             {"selected_groups": [{"slot_id": 3, "degree": 2, "sequence_indices": [4]},
                                  {"slot_id": 5, "degree": 2, "sequence_indices": []}]}]}
+    if name.startswith("fuzz"):
+        return fuzz_plan(name)
     raise FileNotFoundError(name)
+
+
+def fuzz_plan(name):
+    """fuzz<SEED>_n<WORLD>: a random long-tail batch (6-30 sequences of 1-4000 tokens) and a
+    random per-device token capacity, planned now by the kept reference planner (seqplan
+    from baseline/_ref), so groups of every degree, uneven sizes and empty members appear in
+    combinations no committed fixture has."""
+    from paper_2412_01523_b200.planning import import_seqplan
+    import_seqplan()
+    from seqplan.domain import ClusterSpec, CostCoefficients, SequenceBatch
+    from seqplan.workflow import SolveConfig, solve_batch
+    seed, world = name[len("fuzz"):].split("_n")
+    rng = np.random.default_rng(int(seed))
+    n_seq = int(rng.integers(6, 31))
+    lens = [int(x) for x in np.clip(rng.lognormal(6.3, 1.3, size=n_seq), 1, 4000)]
+    coeffs = CostCoefficients(alpha1=1e-9, alpha2=1e-6, beta1=1e-4, alpha3=4096, beta2=1e-5,
+                              m_token=2e4, m_ms=1e6)
+    cap = int(rng.integers(1200, 4001))  # tokens one device holds
+    cluster = ClusterSpec(int(world), 1, 1e15, 2e10, 1e6 + 2e4 * cap)
+    plan = solve_batch(SequenceBatch(tuple(lens), batch_id=name), cluster, coeffs,
+                       SolveConfig(jobs=1))
+    doc = plan.to_json_dict()
+    doc["lengths"] = lens
+    print(json.dumps({"fuzz": name, "lengths": lens, "capacity": cap,
+                      "degrees": [[g["degree"] for g in mb["selected_groups"]]
+                                  for mb in doc["micro_batches"]]}), flush=True)
+    return doc
 
 
 def dense(plan_name, world, H, D):
