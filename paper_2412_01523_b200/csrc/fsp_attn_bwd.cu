@@ -478,7 +478,7 @@ struct BwdSmemV2 {
   static constexpr int kDS = kRing + kSlots * kHalfBytes;  // 2 stages x [128 kv][64 q] bf16
   static constexpr int kStat = kDS + 2 * 16384;       // lse2[2][128], delta[2][128]
   static constexpr int kBar = kStat + 4 * 128 * 4;
-  static constexpr int kBytes = kBar + 256;
+  static constexpr int kBytes = kBar + 512;  // 64 barrier words
 };
 // The fused dK/dV epilogue stages its two 128-row output tiles (2 x 32 KB) in the Q/dO
 // ring, which is idle by then: the ring must hold at least that much.
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* bar_kv = bars + 0;
   constexpr int kR = L::kSlots;
-  static_assert(1 + 2 * kR + 18 <= 32, "barrier region holds 32 mbarriers");
+  static_assert(1 + 2 * kR + 18 <= 64, "barrier region holds 64 words");
   uint64_t* ring_full = bars + 1;            // [kSlots]
   uint64_t* ring_empty = bars + 1 + kR;      // [kSlots]
   uint64_t* s_full = bars + 1 + 2 * kR;      // [2]
