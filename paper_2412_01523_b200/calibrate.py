@@ -9,18 +9,15 @@ pkg/docs/formats.md:62-72).  This module produces those records from the SP step
 on B200: each record is one group executed by FlexSPExecutor, with compute time = the
 group's attention fwd+bwd CUDA-event time (max over its ranks), comm time = its all-to-all
 + barrier time, and memory = the bytes the step allocates per device for that group.
-The fit itself is the reference's own `fit_coefficients` (imported, not re-implemented).
+The fit itself is the reference's own `fit_coefficients` and the CSV its own
+`write_profile_csv` / `ProfileRecord` (imported, not re-implemented).
 """
 from __future__ import annotations
 
-import csv
 from dataclasses import dataclass
 from typing import Sequence
 
 import numpy as np
-
-PROFILE_HEADER = ["tokens", "degree", "bandwidth", "comp_s", "comm_s", "mem_bytes"]
-
 
 @dataclass(frozen=True)
 class GroupMeasurement:
@@ -32,14 +29,17 @@ class GroupMeasurement:
     mem_bytes: float
 
 
+def to_profile_records(rows: Sequence[GroupMeasurement]):
+    """The reference's own ProfileRecord (cost_model.py:47-59) for each measured group."""
+    from seqplan.cost_model import ProfileRecord
+    return [ProfileRecord(tuple(int(s) for s in r.token_lengths), r.degree, r.bandwidth,
+                          r.comp_s, r.comm_s, r.mem_bytes) for r in rows]
+
+
 def write_profile_csv(path, rows: Sequence[GroupMeasurement]) -> None:
-    """Same layout as seqplan.cost_model.write_profile_csv (cost_model.py:283-295)."""
-    with open(path, "w", newline="", encoding="utf-8") as fh:
-        w = csv.writer(fh, delimiter=";", lineterminator="\n")
-        w.writerow(PROFILE_HEADER)
-        for r in rows:
-            w.writerow([",".join(str(int(s)) for s in r.token_lengths), r.degree, r.bandwidth,
-                        r.comp_s, r.comm_s, r.mem_bytes])
+    """The profile CSV through the reference's own writer (cost_model.py:283-295)."""
+    from seqplan.cost_model import write_profile_csv as ref_write
+    ref_write(path, to_profile_records(rows))
 
 
 def step_bytes_per_device(lengths: Sequence[int], degree: int, n_heads: int, head_dim: int) -> float:
@@ -70,10 +70,9 @@ def fit(rows: Sequence[GroupMeasurement], allow_underdetermined: bool = False):
     those rows.  The communication channel is therefore fitted on the d >= 2 records only
     (a second call of the same reference routine) and merged with the compute/memory fit
     of all records.  Returns (FitResult of all records, CostCoefficients merged)."""
-    from seqplan.cost_model import ProfileRecord, fit_coefficients
+    from seqplan.cost_model import fit_coefficients
     from seqplan.domain import CostCoefficients
-    recs = [ProfileRecord(tuple(int(s) for s in r.token_lengths), r.degree, r.bandwidth,
-                          r.comp_s, r.comm_s, r.mem_bytes) for r in rows]
+    recs = to_profile_records(rows)
     full = fit_coefficients(recs, allow_underdetermined=allow_underdetermined)
     multi = [r for r in recs if r.degree > 1]
     c = full.coefficients
