@@ -748,6 +748,20 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       const int lim = p.noncausal ? seqlen - 1 - j * 128 : q_pos - j * 128;
       auto tile_body = [&](auto diag_c) {
         constexpr bool kDiag = decltype(diag_c)::value;
+        // Masking mode of each 32-column chunk of the last kv tile, warp-uniform: 0 = every
+        // lane's columns valid, 2 = every lane's columns masked, 1 = mixed (per-element
+        // selects).  On the causal diagonal a warp's 32 rows need per-element masks in one
+        // chunk only (rows 32q.. see columns <= row): the other chunks take the unmasked
+        // code or are skipped, instead of ~900 compare / select / predicate-shuffle
+        // instructions per row for the whole tile.
+        int cmode[4] = {0, 0, 0, 0};
+        if (kDiag) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            cmode[c] = __all_sync(0xffffffffu, 32 * c + 31 <= lim) ? 0
+                       : __all_sync(0xffffffffu, 32 * c > lim)     ? 2
+                                                                   : 1;
+        }
         // pass 1: row max; four independent FMNMX3 chains over chunked TMEM loads (the
         // whole 128-column row does not fit the 168-register budget of 10 warps per CTA)
         float mxs[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -774,17 +788,23 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           tmem_ld32(tmem + lane_addr + s_col + c, r);
           tmem_ld_wait();
 #endif
+          if (!kDiag || cmode[c / 32] == 0) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8)
+            for (int i = 0; i < 32; i += 8)
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              float v0 = __uint_as_float(r[i + 2 * a]), v1 = __uint_as_float(r[i + 2 * a + 1]);
-              if (kDiag) {
+              for (int a = 0; a < 4; ++a)
+                mxs[a] = fmax3(mxs[a], __uint_as_float(r[i + 2 * a]), __uint_as_float(r[i + 2 * a + 1]));
+          } else if (cmode[c / 32] == 1) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8)
+#pragma unroll
+              for (int a = 0; a < 4; ++a) {
+                float v0 = __uint_as_float(r[i + 2 * a]), v1 = __uint_as_float(r[i + 2 * a + 1]);
                 v0 = c + i + 2 * a <= lim ? v0 : -INFINITY;
                 v1 = c + i + 2 * a + 1 <= lim ? v1 : -INFINITY;
+                mxs[a] = fmax3(mxs[a], v0, v1);
               }
-              mxs[a] = fmax3(mxs[a], v0, v1);
-            }
+          }
 #if FSP_FWD_PREFETCH
           if (c + 32 < 128) tmem_ld_wait_tied(buf[((c / 32) + 1) & 1]);
 #endif
@@ -834,28 +854,34 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           tmem_ld32(tmem + lane_addr + s_col + c, r);
           tmem_ld_wait();
 #endif
+          const int mode = kDiag ? cmode[c / 32] : 0;
+          if (mode == 2) {  // every column of the chunk masked: P = 0
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const uint64_t x2 =
-                ffma2(f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, negm2);
-            float p0, p1;
-            if (kDiag) {
-              float x0, x1;
-              f2_split(x2, x0, x1);
-              p0 = ex2(c + i <= lim ? x0 : -INFINITY);
-              p1 = ex2(c + i + 1 <= lim ? x1 : -INFINITY);
-            } else if (FSP_ABLATE_EXP) {  // profiling ablation: no exponentials
-              f2_split(x2, p0, p1);
-            } else if (FSP_POLY_EVERY > 0 && (i / 2) % FSP_POLY_EVERY == FSP_POLY_EVERY - 1) {
-              ex2_poly2(x2, p0, p1);
-            } else {
-              float x0, x1;
-              f2_split(x2, x0, x1);
-              p0 = ex2(x0);
-              p1 = ex2(x1);
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const uint64_t x2 =
+                  ffma2(f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, negm2);
+              float p0, p1;
+              if (mode == 1) {
+                float x0, x1;
+                f2_split(x2, x0, x1);
+                p0 = ex2(c + i <= lim ? x0 : -INFINITY);
+                p1 = ex2(c + i + 1 <= lim ? x1 : -INFINITY);
+              } else if (FSP_ABLATE_EXP) {  // profiling ablation: no exponentials
+                f2_split(x2, p0, p1);
+              } else if (FSP_POLY_EVERY > 0 && (i / 2) % FSP_POLY_EVERY == FSP_POLY_EVERY - 1) {
+                ex2_poly2(x2, p0, p1);
+              } else {
+                float x0, x1;
+                f2_split(x2, x0, x1);
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+              }
+              sum2[(i >> 1) & 3] = fadd2(sum2[(i >> 1) & 3], f2(p0, p1));
+              pk[i / 2] = pack_bf16(p0, p1);
             }
-            sum2[(i >> 1) & 3] = fadd2(sum2[(i >> 1) & 3], f2(p0, p1));
-            pk[i / 2] = pack_bf16(p0, p1);
           }
           tmem_st16(tmem + lane_addr + s_col + c / 2, pk);
           if (c == 32) {  // P for kv rows 0..63 is in TMEM: release the first PV half
