@@ -23,7 +23,8 @@ def main():
             cur = next(names, line.split()[-1])
             cur = re.sub(r"^void ", "", cur)
             cur = cur.replace("fsp::(anonymous namespace)::", "").replace("fsp::<unnamed>::", "")
-            cur = cur.replace("(bool)0", "false").replace("(bool)1", "true").split("(")[0]
+            cur = cur.replace("(bool)0", "false").replace("(bool)1", "true")
+            cur = re.sub(r"\((?:int|unsigned int|long)\)", "", cur).split("(")[0]
             counts[cur] = {o: 0 for o in OPS}
             continue
         m = re.match(r"\s*/\*[0-9a-f]+\*/\s+(?:@!?U?P\w+\s+)?([A-Z0-9_.]+)", line)
