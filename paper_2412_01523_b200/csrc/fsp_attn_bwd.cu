@@ -861,6 +861,14 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       }
       tmem_ld_wait();
       uint32_t pk[kV2Cols / 2], dk[kV2Cols / 2];
+      // masked unit: warp-uniform mode of this warp's kV2Cols columns — 0 all valid (the
+      // unmasked code), 2 all masked (P = dS = 0, no exponentials), 1 mixed (per element)
+      int mode = 0;
+      if (kDiag) {
+        const bool all_valid = p.noncausal ? !kv_dead : c0 >= r;
+        const bool all_masked = p.noncausal ? kv_dead : c0 + kV2Cols - 1 < r;
+        mode = __all_sync(0xffffffffu, all_valid) ? 0 : __all_sync(0xffffffffu, all_masked) ? 2 : 1;
+      }
       const uint64_t sl2x2 = f2(sl2, sl2);
       const uint64_t* nls2 = reinterpret_cast<const uint64_t*>(ls);  // -lse*log2e pairs
       const uint64_t* dl2 = reinterpret_cast<const uint64_t*>(dl);
@@ -876,6 +884,10 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       const float ls_lane = lane < (uint32_t)kV2Cols ? ls[lane] : 0.f;
       const float dl_lane = lane < (uint32_t)kV2Cols ? dl[lane] : 0.f;
 #endif
+      if (mode == 2) {
+#pragma unroll
+        for (int i = 0; i < kV2Cols / 2; ++i) pk[i] = dk[i] = 0u;
+      } else
 #pragma unroll
       for (int i = 0; i < kV2Cols; i += 2) {
         const uint64_t x2 =
@@ -895,7 +907,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
           p0 = ex2(x0);
           p1 = ex2(x1);
         }
-        if (kDiag) {
+        if (kDiag && mode == 1) {
           if (p.noncausal) {  // the last, partial kv tile: rows past the sequence end
             if (kv_dead) p0 = p1 = 0.f;
           } else {  // causal on the diagonal tile: query column c0+i >= kv row r
