@@ -6,7 +6,7 @@ export CUDA_DEVICE_MAX_CONNECTIONS=32 CUDA_MODULE_LOADING=EAGER FSP_BARRIER_TIME
 heads=(5 6 7 8 9 10 12 13 16)
 pass=0; fail=0; rej=0
 for s in $(seq $1 $2); do
-  w=$(( s % 2 == 0 ? 4 : 8 )); h=${heads[$(( s % ${#heads[@]} ))]}; d=$(( s % 5 == 0 ? 64 : 128 ))
+  w=$(( s % 3 == 0 ? 2 : (s % 3 == 1 ? 4 : 8) )); h=${heads[$(( s % ${#heads[@]} ))]}; d=$(( s % 5 == 0 ? 64 : 128 ))
   out=$(timeout 300 python tests/vrank_parity.py dense fuzz${s}_n$w $w $h $d 2>&1)
   rc=$?
   plan=$(echo "$out" | grep '^{"fuzz"' | head -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read() or "{}"); print(d.get("degrees"), len(d.get("lengths", [])), sum(d.get("lengths", [])))' 2>/dev/null)
